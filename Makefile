@@ -1,0 +1,36 @@
+# Builds the in-tree C-ABI library paper_1805_01407_b200/_lib/libslp_b200.so
+# (sm_100a only) and the CPU oracle oracle/_build/liboracle.so (test-only).
+NVCC ?= /usr/local/cuda/bin/nvcc
+CSRC := paper_1805_01407_b200/csrc
+LIBDIR := paper_1805_01407_b200/_lib
+OBJDIR := build/obj
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall -Xptxas -v -I include
+CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -I include
+
+INST := $(wildcard $(CSRC)/slp_inst_*.cu)
+OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(INST)) $(OBJDIR)/slp_api.o $(OBJDIR)/slp_host.o
+HDRS := $(wildcard $(CSRC)/*.h $(CSRC)/*.cuh) include/slp_b200.h
+
+all: $(LIBDIR)/libslp_b200.so oracle
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ > $@.ptxas.log 2>&1 || (cat $@.ptxas.log; false)
+
+$(OBJDIR)/slp_host.o: $(CSRC)/slp_host.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	g++ $(CXXFLAGS) -c $< -o $@
+
+$(LIBDIR)/libslp_b200.so: $(OBJS)
+	@mkdir -p $(LIBDIR)
+	$(NVCC) -shared $(ARCH) -cudart static -o $@ $(OBJS)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIBDIR)/*.so
+	$(MAKE) -C oracle clean
+
+.PHONY: all clean oracle

@@ -1,0 +1,153 @@
+/*
+ * slp_b200.h -- C ABI of the B200-native bulk generator for the scrambled
+ * linear generators of Blackman & Vigna (arXiv 1805.01407).
+ *
+ * The reference (`slprng`, pure Python) has no FFI; every entry point below
+ * replaces one reference function on the bulk `next()` path, cited as
+ * file:line relative to /root/reference/pkg/src/slprng/.  Plain pointers and
+ * sizes only: no torch types cross this boundary.  Device pointers are
+ * caller-owned (e.g. torch CUDA tensors); `stream` is a cudaStream_t passed
+ * as void* (NULL = legacy default stream).
+ *
+ * Every function returns SLP_OK (0) or a negative slp_status.  The Python
+ * layer maps SLP_ERR_INVALID / SLP_ERR_ZERO_STATE / SLP_ERR_ENGINE_MISMATCH to
+ * ValueError, SLP_ERR_UNKNOWN_GENERATOR to KeyError and SLP_ERR_ALGEBRA to
+ * Gf2Error, matching generators.py:120-124,194-215,315-323 and gf2.py:48-53.
+ *
+ * State layout on the device ("SoA"): word j of substream i lives at
+ * states[j * ld + i], j < k, in the FLAT word order of engines.py:14-18,
+ * as uint64 for w = 64 generators and uint32 for w = 32 generators.
+ */
+#ifndef SLP_B200_H
+#define SLP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum slp_status {
+  SLP_OK = 0,
+  SLP_ERR_INVALID = -1,           /* ValueError: bad argument / parameter      */
+  SLP_ERR_UNKNOWN_GENERATOR = -2, /* KeyError: unknown name or id              */
+  SLP_ERR_UNSUPPORTED = -3,       /* combination the device path does not do   */
+  SLP_ERR_ZERO_STATE = -4,        /* ValueError: all-zero state / zero jump    */
+  SLP_ERR_CUDA = -5,              /* CUDA runtime error (see slp_last_error)   */
+  SLP_ERR_ALGEBRA = -6,           /* Gf2Error: internal self-check failed      */
+  SLP_ERR_BUFFER = -7             /* output buffer too small                   */
+} slp_status;
+
+/* Output element kinds for slp_fill. */
+typedef enum slp_out_kind {
+  SLP_OUT_NATIVE = 0, /* w-bit words: uint64 (w=64) or uint32 (w=32)             */
+  SLP_OUT_U64 = 1,    /* uint64, 32-bit outputs zero-extended (generators.py:474) */
+  SLP_OUT_F64 = 2,    /* double (x >> 11) * 2^-53, w = 64 (generators.py:307-311) */
+  SLP_OUT_F32 = 3     /* float (x >> 8) * 2^-24, w = 32 (north_star; no ref fn)    */
+} slp_out_kind;
+
+/* Output layouts for slp_fill. */
+typedef enum slp_layout {
+  SLP_STREAM_MAJOR = 0,  /* out[i * ld_out + t]: substream i, position t         */
+  SLP_POSITION_MAJOR = 1 /* out[t * ld_out + i]: the (T, L) buffer of generators.py:474 */
+} slp_layout;
+
+/* Consumer flags for slp_fused. */
+typedef enum slp_fuse_flags {
+  SLP_FUSE_INT = 1, /* wrapping sum, xor, exact sum of x and of the low bits        */
+  SLP_FUSE_F64 = 2  /* additionally a real float64 accumulation of the converted values */
+} slp_fuse_flags;
+
+typedef struct slp_gen_info {
+  int32_t id, family, k, w, a, b, c; /* family: 0 xoroshiro, 1 xoshiro, 2 xorshift */
+  int32_t scrambler, word_i, word_j, R;   /* scrambler: 0 none 1 + 2 * 3 ++ 4 ** */
+  uint64_t S, T;
+  char name[32];
+} slp_gen_info;
+
+/* Result of the fused consumer.  All integer fields are exact and independent
+ * of summation order; `mant` = (sum - low_sum) >> shift is the exact integer
+ * sum of (x >> shift), shift = 11 (w=64) or 8 (w=32), so the float64 sum of
+ * the converted values is mant * 2^-(53|24) rounded once. */
+typedef struct slp_checksum {
+  uint64_t sum_lo;  /* sum of outputs mod 2^64 (the wrapping checksum)          */
+  uint64_t sum_hi;  /* bits 64..127 of the exact sum of outputs                  */
+  uint64_t xor_all; /* xor of all outputs                                        */
+  uint64_t low_sum; /* exact sum of (x & (2^shift - 1))                           */
+  uint64_t count;   /* number of outputs consumed                                */
+  double fsum;      /* float64 accumulation of converted values (SLP_FUSE_F64)   */
+} slp_checksum;
+
+/* ---- registry: generators.py:71-124 ------------------------------------ */
+int slp_num_generators(void);
+/* id of a registry name, or SLP_ERR_UNKNOWN_GENERATOR (get_spec, generators.py:120-124) */
+int slp_generator_id(const char *name);
+int slp_generator_info(int id, slp_gen_info *out);
+
+/* ---- host GF(2) algebra (setup; not per output) ------------------------- */
+/* characteristic polynomial of the engine step matrix, bit i = coeff of x^i,
+ * little-endian words; replaces engine_char_poly (generators.py:387-394,
+ * gf2.py:418-469).  poly_words >= n/64 + 1. */
+int slp_char_poly(int id, uint64_t *poly, int poly_words);
+/* x^steps mod P, steps a little-endian multiword integer; replaces
+ * compute_jump_poly (generators.py:397-402, gf2.py:214-227). */
+int slp_jump_poly(int id, const uint64_t *steps, int steps_words, uint64_t *poly, int poly_words);
+/* scalar jump of one flat state (k words, each < 2^w) on the host; replaces
+ * Generator.jump (generators.py:315-334). */
+int slp_host_jump(int id, const uint64_t *poly, int poly_words, uint64_t *flat_state);
+
+/* Same for an arbitrary engine (custom_spec, generators.py:127-135):
+ * family 0 xoroshiro / 1 xoshiro / 2 xorshift, k*w <= 1024, w <= 64.
+ * Validation follows EngineKind / _check_params (engines.py:56-97). */
+int slp_engine_char_poly(int family, int k, int w, int a, int b, int c, uint64_t *poly, int poly_words);
+int slp_engine_jump_poly(int family, int k, int w, int a, int b, int c, const uint64_t *steps, int steps_words,
+                         uint64_t *poly, int poly_words);
+
+/* ---- device: substream initialisation (kernel K1) ----------------------- */
+/* For each block b < nblocks and substream i < n:
+ *   states[b*n + i] = base_b * M^(i * steps)
+ * where base_b = base_flat[b*k .. b*k+k) (host memory, flat words) and
+ * `steps` is the little-endian multiword stride (2^(n/2) for jump()).
+ * Replaces the LanedStream lane doubling (generators.py:450-459) and
+ * Generator.jump + compute_jump_poly for stream i (generators.py:315-334,397-402).
+ * ld >= nblocks * n. */
+int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, const uint64_t *steps,
+                        int steps_words, void *states, uint64_t ld, uint64_t n, void *stream);
+/* dst[i] = src[i] * p(M) for i < count (one polynomial for every state);
+ * replaces LanedStream._vec_jump (generators.py:493-505) and the super-jump
+ * between superbatches (:487-490).  src may equal dst. */
+int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *src, uint64_t ld_src,
+                    void *dst, uint64_t ld_dst, uint64_t count, void *stream);
+
+/* ---- device: bulk generation (kernels K2/K3/K5) ------------------------- */
+/* Emits T outputs of each of nstreams substreams (scramble current state,
+ * then step: Generator.next, generators.py:244-305) into `out`, converting
+ * per out_kind, and writes the advanced states to states_out (may equal
+ * states_in; NULL = do not write back).  ld_out = row pitch in elements
+ * (>= T for stream-major, >= nstreams for position-major).  Replaces
+ * LanedStream.chunks (generators.py:465-490; VecStepper.step engines.py:318-361;
+ * ScramblerSpec.apply_vec scramblers.py:97-127; buf.T.flatten :482). */
+int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams,
+             uint64_t T, int out_kind, int layout, void *out, uint64_t ld_out, void *stream);
+
+/* ---- device: fused consumer (kernel K4) ---------------------------------- */
+/* Same outputs as slp_fill, reduced in-kernel instead of stored; writes one
+ * slp_checksum to result (DEVICE memory).  workspace: device scratch of
+ * slp_fused_workspace_bytes(nstreams) bytes. */
+size_t slp_fused_workspace_bytes(int id, uint64_t nstreams);
+int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams,
+              uint64_t T, int flags, void *result, void *workspace, size_t workspace_bytes,
+              void *stream);
+
+/* ---- misc ---------------------------------------------------------------- */
+const char *slp_status_str(int status);
+/* last CUDA error string seen by this thread ("" if none) */
+const char *slp_last_error(void);
+/* library version / build info */
+const char *slp_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLP_B200_H */

@@ -1,0 +1,387 @@
+// C ABI (device part): dispatch to the per-generator kernel instances,
+// substream-initialisation driver (K1), TMA descriptor set-up and the final
+// deterministic reduction of the fused consumer (K4).
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <stdexcept>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "slp_device.cuh"
+#include "slp_internal.h"
+
+#define SLP_PART_DECL(P) extern const ::slp::GenOps slp_ops_part_##P[SLP_NUM_GENERATORS];
+SLP_PART_DECL(0)
+SLP_PART_DECL(1)
+SLP_PART_DECL(2)
+SLP_PART_DECL(3)
+SLP_PART_DECL(4)
+SLP_PART_DECL(5)
+
+namespace slp {
+
+const GenOps *gen_ops(int id) {
+  static GenOps table[SLP_NUM_GENERATORS];
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const GenOps *parts[] = {slp_ops_part_0, slp_ops_part_1, slp_ops_part_2,
+                             slp_ops_part_3, slp_ops_part_4, slp_ops_part_5};
+    for (int i = 0; i < SLP_NUM_GENERATORS; ++i)
+      for (const GenOps *p : parts)
+        if (p[i].fill) table[i] = p[i];
+  });
+  if (id < 0 || id >= SLP_NUM_GENERATORS || !table[id].fill) return nullptr;
+  return &table[id];
+}
+
+int current_device() {
+  int d = -1;
+  if (cudaGetDevice(&d) != cudaSuccess) return -1;
+  return d;
+}
+
+int sm_count(int dev) {
+  static int cache[64] = {0};
+  if (dev < 0 || dev >= 64) return 1;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 1;
+  }
+  return cache[dev];
+}
+
+static int env_int(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// tuning knobs (read once): SLP_FILL_GRID_MULT, SLP_STORE_PATH (0 auto, 1 TMA, 2 staged)
+int fill_grid_mult() {
+  static int v = env_int("SLP_FILL_GRID_MULT", 1);
+  return v > 0 ? v : 1;
+}
+
+int cuda_fail(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  set_last_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return SLP_ERR_CUDA;
+}
+
+int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_last_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return SLP_ERR_CUDA;
+  }
+  return SLP_OK;
+}
+
+bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out) {
+  static int path = env_int("SLP_STORE_PATH", 0);
+  if (path == 2) return false;
+  const uint64_t ch = 128 / es;
+  return ((uintptr_t)out % 16) == 0 && (ld_out * es) % 16 == 0 && T >= ch && T < (1ull << 31) &&
+         nstreams < (1ull << 31) && ld_out * es < (1ull << 40) && ld_out >= T;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return SLP_ERR_CUDA;
+  }
+  cuuint64_t gdim[2] = {(cuuint64_t)T, (cuuint64_t)nstreams};
+  cuuint64_t gstride[1] = {(cuuint64_t)(ld_out * es)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / es), 32};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = fn(map, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, gdim,
+                  gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return SLP_ERR_CUDA;
+  }
+  return SLP_OK;
+}
+
+namespace dev {
+__global__ void k_fused_final(const slp_checksum *parts, int nparts, slp_checksum *result, uint64_t count,
+                              double fscale) {
+  __shared__ uint64_t s_lo[256], s_hi[256], s_x[256], s_low[256];
+  __shared__ double s_f[256];
+  const int t = threadIdx.x;
+  uint64_t lo = 0, hi = 0, x = 0, low = 0;
+  double f = 0.0;
+  for (int i = t; i < nparts; i += 256) {
+    const slp_checksum c = parts[i];
+    const uint64_t nlo = lo + c.sum_lo;
+    hi += c.sum_hi + (nlo < lo ? 1 : 0);
+    lo = nlo;
+    x ^= c.xor_all;
+    low += c.low_sum;
+    f += c.fsum;
+  }
+  s_lo[t] = lo;
+  s_hi[t] = hi;
+  s_x[t] = x;
+  s_low[t] = low;
+  s_f[t] = f;
+  __syncthreads();
+  if (t == 0) {
+    for (int i = 1; i < 256; ++i) {
+      const uint64_t nlo = lo + s_lo[i];
+      hi += s_hi[i] + (nlo < lo ? 1 : 0);
+      lo = nlo;
+      x ^= s_x[i];
+      low += s_low[i];
+      f += s_f[i];
+    }
+    result->sum_lo = lo;
+    result->sum_hi = hi;
+    result->xor_all = x;
+    result->low_sum = low;
+    result->count = count;
+    result->fsum = f * fscale;
+  }
+}
+}  // namespace dev
+
+// device copies of the init-plan polynomials, per (plan, device)
+static std::mutex g_dev_mu;
+static std::map<std::pair<const InitPlan *, int>, void *> g_dev_polys;
+
+static int plan_polys_on_device(const InitPlan &plan, int dev, const uint64_t **out) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto key = std::make_pair(&plan, dev);
+  auto it = g_dev_polys.find(key);
+  if (it != g_dev_polys.end()) {
+    *out = static_cast<const uint64_t *>(it->second);
+    return SLP_OK;
+  }
+  void *d = nullptr;
+  const size_t bytes = plan.polys.size() * sizeof(uint64_t);
+  if (cudaMalloc(&d, bytes) != cudaSuccess) return cuda_fail("cudaMalloc(init polys)");
+  if (cudaMemcpy(d, plan.polys.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail("cudaMemcpy(init polys)");
+  }
+  g_dev_polys[key] = d;
+  *out = static_cast<const uint64_t *>(d);
+  return SLP_OK;
+}
+
+}  // namespace slp
+
+using namespace slp;
+
+static bool state_ok(const GenDesc &g, const uint64_t *words) {
+  const uint64_t mask = g.w == 64 ? ~0ull : ((1ull << g.w) - 1);
+  bool any = false;
+  for (int j = 0; j < g.k; ++j) {
+    if (words[j] & ~mask) return false;
+    any |= words[j] != 0;
+  }
+  return any;
+}
+
+extern "C" {
+
+int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, const uint64_t *steps, int steps_words,
+                        void *states, uint64_t ld, uint64_t n, void *stream) {
+  const GenDesc *g = gen_desc(id);
+  if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
+  const GenOps *ops = gen_ops(id);
+  if (!ops) return SLP_ERR_UNSUPPORTED;
+  if (!base_flat || !states || nblocks == 0 || n == 0 || ld < nblocks * n || steps_words < 0 ||
+      (steps_words > 0 && !steps) || nblocks > 65535)
+    return SLP_ERR_INVALID;
+  for (uint64_t b = 0; b < nblocks; ++b)
+    if (!state_ok(*g, base_flat + b * g->k)) return SLP_ERR_ZERO_STATE;
+  const InitPlan *plan;
+  try {
+    plan = &init_plan(id, steps, steps_words, n);
+  } catch (const AlgebraError &e) {
+    set_last_error(e.what());
+    return SLP_ERR_ALGEBRA;
+  } catch (const std::exception &e) {
+    set_last_error(e.what());
+    return SLP_ERR_INVALID;
+  }
+  const int dev = current_device();
+  if (dev < 0) return cuda_fail("cudaGetDevice");
+  const uint64_t *d_polys = nullptr;
+  int rc = plan_polys_on_device(*plan, dev, &d_polys);
+  if (rc != SLP_OK) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t esize = g->w / 8;
+  // launch 0: every block base -> first m0 substreams (one polynomial per substream)
+  const InitLaunch &l0 = plan->launches[0];
+  for (uint64_t b0 = 0; b0 < nblocks; b0 += kMaxBaseBatches) {
+    const uint64_t nb = nblocks - b0 < (uint64_t)kMaxBaseBatches ? nblocks - b0 : (uint64_t)kMaxBaseBatches;
+    BaseStates base;
+    std::memset(&base, 0, sizeof base);
+    for (uint64_t b = 0; b < nb; ++b)
+      for (int j = 0; j < g->k; ++j) base.w[b * g->k + j] = base_flat[(b0 + b) * g->k + j];
+    JumpParams p{};
+    p.src = nullptr;
+    p.dst = static_cast<uint8_t *>(states) + b0 * n * esize;
+    p.ld_dst = ld;
+    p.polys = d_polys;
+    p.poly0 = l0.poly0;
+    p.pmode = 2;
+    p.use_base = 1;
+    p.count = l0.count;
+    p.m = 0;
+    p.dst_off = 0;
+    p.batch_stride = n;
+    rc = ops->jump(p, &base, false, nb, st);
+    if (rc != SLP_OK) return rc;
+  }
+  for (size_t li = 1; li < plan->launches.size(); ++li) {
+    const InitLaunch &L = plan->launches[li];
+    JumpParams p{};
+    p.src = states;
+    p.ld_src = ld;
+    p.dst = states;
+    p.ld_dst = ld;
+    p.polys = d_polys;
+    p.poly0 = L.poly0;
+    p.pmode = 1;
+    p.use_base = 0;
+    p.count = L.count;
+    p.m = L.m;
+    p.src_off = 0;
+    p.dst_off = L.dst0;
+    p.batch_stride = n;
+    rc = ops->jump(p, nullptr, L.uniform, nblocks, st);
+    if (rc != SLP_OK) return rc;
+  }
+  return SLP_OK;
+}
+
+int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *src, uint64_t ld_src, void *dst,
+                    uint64_t ld_dst, uint64_t count, void *stream) {
+  const GenDesc *g = gen_desc(id);
+  if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
+  const GenOps *ops = gen_ops(id);
+  if (!ops) return SLP_ERR_UNSUPPORTED;
+  if (!poly || poly_words <= 0 || !src || !dst || ld_src < count || ld_dst < count) return SLP_ERR_INVALID;
+  const int pw = g->n() / 64;
+  bool nonzero = false;
+  for (int i = 0; i < poly_words; ++i) {
+    if (i >= pw && poly[i]) return SLP_ERR_INVALID;  // degree must be < n (reduced mod P)
+    nonzero |= poly[i] != 0;
+  }
+  if (!nonzero) return SLP_ERR_ZERO_STATE;
+  BaseStates base;
+  std::memset(&base, 0, sizeof base);
+  for (int i = 0; i < pw && i < poly_words; ++i) base.w[i] = poly[i];
+  JumpParams p{};
+  p.src = src;
+  p.ld_src = ld_src;
+  p.dst = dst;
+  p.ld_dst = ld_dst;
+  p.polys = nullptr;  // polynomial in the BaseStates parameter block
+  p.poly0 = 0;
+  p.pmode = 0;
+  p.use_base = 0;
+  p.count = count;
+  p.m = 0;
+  p.batch_stride = 0;
+  if (src == dst) {
+    // in place: k_jump reads all words of a state before writing them
+  }
+  return ops->jump(p, &base, true, 1, static_cast<cudaStream_t>(stream));
+}
+
+int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams, uint64_t T,
+             int out_kind, int layout, void *out, uint64_t ld_out, void *stream) {
+  const GenDesc *g = gen_desc(id);
+  if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
+  const GenOps *ops = gen_ops(id);
+  if (!ops) return SLP_ERR_UNSUPPORTED;
+  if (!states_in || ld < nstreams || (!out && T && nstreams)) return SLP_ERR_INVALID;
+  if (layout == SLP_STREAM_MAJOR && ld_out < T) return SLP_ERR_INVALID;
+  if (layout == SLP_POSITION_MAJOR && ld_out < nstreams) return SLP_ERR_INVALID;
+  if (nstreams >= (1ull << 40)) return SLP_ERR_INVALID;
+  FillParams p{};
+  p.sin = states_in;
+  p.sout = states_out;
+  p.ld = ld;
+  p.nstreams = nstreams;
+  p.T = T;
+  p.out = out;
+  p.ld_out = ld_out;
+  if (nstreams == 0) return SLP_OK;
+  if (T == 0) {
+    if (states_out && states_out != states_in) {
+      const size_t es = g->w / 8;
+      for (int j = 0; j < g->k; ++j)
+        if (cudaMemcpyAsync(static_cast<uint8_t *>(states_out) + j * ld * es,
+                            static_cast<const uint8_t *>(states_in) + j * ld * es, nstreams * es,
+                            cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+          return cuda_fail("cudaMemcpyAsync(states)");
+    }
+    return SLP_OK;
+  }
+  return ops->fill(p, out_kind, layout, static_cast<cudaStream_t>(stream));
+}
+
+size_t slp_fused_workspace_bytes(int id, uint64_t nstreams) {
+  (void)nstreams;
+  const GenOps *ops = gen_ops(id);
+  if (!ops) return 0;
+  const int dev = current_device();
+  if (dev < 0) return 0;
+  return (size_t)ops->fused_grid_cap(dev) * sizeof(slp_checksum);
+}
+
+int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams, uint64_t T, int flags,
+              void *result, void *workspace, size_t workspace_bytes, void *stream) {
+  const GenDesc *g = gen_desc(id);
+  if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
+  const GenOps *ops = gen_ops(id);
+  if (!ops) return SLP_ERR_UNSUPPORTED;
+  if (!states_in || !result || !workspace || ld < nstreams || !(flags & (SLP_FUSE_INT | SLP_FUSE_F64)))
+    return SLP_ERR_INVALID;
+  FusedParams p{};
+  p.sin = states_in;
+  p.sout = states_out;
+  p.ld = ld;
+  p.nstreams = nstreams;
+  p.T = T;
+  p.partials = workspace;
+  p.workspace_bytes = workspace_bytes;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int grid = 0;
+  int rc = ops->fused(p, flags, st, &grid);
+  if (rc != SLP_OK) return rc;
+  const double fscale = g->w == 64 ? 0x1.0p-53 : 0x1.0p-24;
+  dev::k_fused_final<<<1, 256, 0, st>>>(static_cast<const slp_checksum *>(workspace), grid,
+                                        static_cast<slp_checksum *>(result), nstreams * T, fscale);
+  return check_launch("k_fused_final");
+}
+
+const char *slp_build_info(void) {
+  return "slp_b200 sm_100a (tcgen05-free integer path; TMA bulk tensor stores) built " __DATE__ " " __TIME__;
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// Launch-parameter structs and the per-generator dispatch table shared by the
+// kernel instantiation units (slp_inst_*.cu) and the C ABI (slp_api.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace slp {
+
+struct FillParams {
+  const void *sin;   // SoA states [k][ld]
+  void *sout;        // may alias sin; nullptr = no write-back
+  uint64_t ld;
+  uint64_t nstreams;
+  uint64_t T;
+  void *out;
+  uint64_t ld_out;
+  uint64_t nunits;   // filled by the launcher
+};
+
+struct FusedParams {
+  const void *sin;
+  void *sout;
+  uint64_t ld;
+  uint64_t nstreams;
+  uint64_t T;
+  void *partials;          // slp_checksum[grid]
+  size_t workspace_bytes;  // bytes available at partials
+  uint64_t nunits;
+};
+
+struct JumpParams {
+  const void *src;
+  uint64_t ld_src;
+  void *dst;
+  uint64_t ld_dst;
+  const uint64_t *polys;  // device, G::pw words per polynomial
+  uint64_t poly0;
+  int pmode;              // 0: poly0 for all, 1: poly0 + t / m, 2: poly0 + t
+  int use_base;           // source state = BaseStates entry of the batch
+  uint64_t count;         // states per batch
+  uint64_t m;             // source index t % m (0: t)
+  uint64_t src_off, dst_off, batch_stride;
+};
+
+// up to 16 batches (long-jump blocks) x 16 words, passed by value
+constexpr int kMaxBaseBatches = 16;
+struct BaseStates {
+  uint64_t w[kMaxBaseBatches * 16];
+};
+
+struct GenOps {
+  int (*fill)(const FillParams &, int out_kind, int layout, cudaStream_t);
+  int (*fused)(const FusedParams &, int flags, cudaStream_t, int *grid_out);
+  int (*fused_grid_cap)(int dev);
+  int (*jump)(const JumpParams &, const BaseStates *, bool uniform, uint64_t nbatch, cudaStream_t);
+};
+
+const GenOps *gen_ops(int id);
+
+// helpers implemented in slp_api.cu
+int current_device();
+int sm_count(int dev);
+int fill_grid_mult();
+int cuda_fail(const char *what);
+int check_launch(const char *what);
+bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out);
+int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out);
+
+}  // namespace slp

@@ -1,0 +1,292 @@
+"""Device-resident substreams and the bulk fill / fused-consumer API.
+
+``Substreams`` holds the states of many independent substreams of one
+generator on a GPU, in the SoA layout of include/slp_b200.h ((k, ld) words,
+flat word order, uint64 for w = 64 and uint32 for w = 32).  Substream i of
+block b starts at  base * M^(b * block_stride + i * stride)  — with the
+defaults stride = 2^(n/2) (``jump()``) and block_stride = 2^(3n/4)
+(``long_jump``), i.e. exactly the states the reference reaches with
+``Generator.jump`` / ``compute_jump_poly`` (generators.py:315-334, :397-419)
+and ``LanedStream`` lane set-up (:435-463).
+
+Everything here runs through the C ABI (kernels K1, K2/K3, K4); torch only
+supplies device memory and the current CUDA stream.  There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .generators import Generator, GeneratorSpec, JumpPolynomial, compute_jump_poly, native_id
+
+__all__ = ["Substreams", "Checksum", "fill", "fused_checksum", "require_cuda"]
+
+_KIND = {"native": _native.OUT_NATIVE, "u64": _native.OUT_U64, "f64": _native.OUT_F64, "f32": _native.OUT_F32}
+_LAYOUT = {"stream": _native.STREAM_MAJOR, "position": _native.POSITION_MAJOR}
+
+
+def require_cuda(device=None) -> torch.device:
+    """The CUDA device to use; raises if there is none (no CPU fallback)."""
+    _native.lib()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1805_01407_b200 bulk generation requires a CUDA device (sm_100a); none found")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def _stream_ptr(dev: torch.device):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _word_dtype(w: int):
+    return torch.uint64 if w == 64 else torch.uint32
+
+
+def _out_dtype(spec: GeneratorSpec, kind: str):
+    w = spec.kind.w
+    if kind == "native":
+        return _word_dtype(w)
+    if kind == "u64":
+        return torch.uint64
+    if kind == "f64":
+        if w != 64:
+            raise ValueError("f64 output requires a 64-bit generator (generators.py:309-310)")
+        return torch.float64
+    if kind == "f32":
+        if w != 32:
+            raise ValueError("f32 output (x >> 8) * 2^-24 is defined for 32-bit generators")
+        return torch.float32
+    raise ValueError(f"unknown output kind {kind!r}")
+
+
+@dataclass(frozen=True)
+class Checksum:
+    """Exact reduction of a set of outputs (see slp_checksum in include/slp_b200.h)."""
+
+    w: int
+    sum: int        # wrapping sum mod 2^64
+    sum_exact: int  # exact integer sum
+    xor: int
+    mant: int       # exact sum of (x >> 11) (w=64) / (x >> 8) (w=32)
+    count: int
+    fsum_f64: float | None  # float64 accumulation in the kernel (summation order differs)
+
+    @property
+    def fsum(self) -> float:
+        """mant * 2^-53 (w=64) / 2^-24 (w=32), correctly rounded once."""
+        from fractions import Fraction
+
+        return float(Fraction(self.mant, 1 << (53 if self.w == 64 else 24)))
+
+    @classmethod
+    def from_raw(cls, raw: _native.Checksum, w: int, with_f64: bool):
+        exact = (int(raw.sum_hi) << 64) | int(raw.sum_lo)
+        shift = 11 if w == 64 else 8
+        return cls(w, int(raw.sum_lo), exact, int(raw.xor_all), (exact - int(raw.low_sum)) >> shift,
+                   int(raw.count), float(raw.fsum) if with_f64 else None)
+
+    @classmethod
+    def fold(cls, parts):
+        """Combine checksums of disjoint output sets (order-independent, exact)."""
+        parts = list(parts)
+        w = parts[0].w
+        exact = sum(p.sum_exact for p in parts)
+        x = 0
+        for p in parts:
+            x ^= p.xor
+        f64 = None
+        if all(p.fsum_f64 is not None for p in parts):
+            f64 = float(sum(p.fsum_f64 for p in parts))
+        return cls(w, exact & ((1 << 64) - 1), exact, x, sum(p.mant for p in parts),
+                   sum(p.count for p in parts), f64)
+
+
+def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor | None = None,
+         kind: str = "native", layout: str = "stream", nstreams: int | None = None,
+         states_out: torch.Tensor | None = None, advance: bool = True) -> torch.Tensor:
+    """Kernel K2/K3: T outputs of each substream whose SoA states are ``states``
+    ((k, ld) words).  Returns ``out`` of shape (nstreams, T) (stream-major) or
+    (T, nstreams) (position-major).  States advance in place unless
+    ``advance=False`` or ``states_out`` is given."""
+    gid = native_id(spec)
+    k = spec.kind.k
+    if states.dim() != 2 or states.shape[0] != k or states.dtype != _word_dtype(spec.kind.w) or not states.is_cuda:
+        raise ValueError(f"states must be a CUDA ({k}, ld) {_word_dtype(spec.kind.w)} tensor")
+    if not states.is_contiguous():
+        raise ValueError("states must be contiguous")
+    ld = states.shape[1]
+    n = ld if nstreams is None else int(nstreams)
+    if T < 0 or n < 0 or n > ld:
+        raise ValueError("bad T / nstreams")
+    dt = _out_dtype(spec, kind)
+    if layout not in _LAYOUT:
+        raise ValueError(f"unknown layout {layout!r}")
+    shape = (n, T) if layout == "stream" else (T, n)
+    if out is None:
+        out = torch.empty(shape, dtype=dt, device=states.device)
+    elif out.dtype != dt or out.device != states.device or out.dim() != 2 or out.stride(1) != 1 \
+            or tuple(out.shape) != shape:
+        raise ValueError(f"out must be a {shape} {dt} tensor on {states.device} with unit inner stride")
+    ld_out = out.stride(0) if out.shape[0] > 1 else shape[1]
+    if states_out is None:
+        sout = states.data_ptr() if advance else None
+    else:
+        if states_out.shape != states.shape or states_out.dtype != states.dtype:
+            raise ValueError("states_out must match states")
+        sout = states_out.data_ptr()
+    L = _native.lib()
+    with torch.cuda.device(states.device):
+        rc = L.slp_fill(gid, ctypes.c_void_p(states.data_ptr()), ctypes.c_void_p(sout), ld, n, T,
+                        _KIND[kind], _LAYOUT[layout], ctypes.c_void_p(out.data_ptr()), ld_out,
+                        _stream_ptr(states.device))
+    _native.check(rc, "fill")
+    return out
+
+
+_workspaces: dict = {}
+
+
+def _workspace(gid: int, dev: torch.device) -> torch.Tensor:
+    key = (gid, dev.index)
+    ws = _workspaces.get(key)
+    if ws is None:
+        with torch.cuda.device(dev):
+            nbytes = int(_native.lib().slp_fused_workspace_bytes(gid, 0))
+        ws = torch.empty(max(nbytes, 64), dtype=torch.uint8, device=dev)
+        _workspaces[key] = ws
+    return ws
+
+
+def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, f64: bool = False,
+                         nstreams: int | None = None, advance: bool = True,
+                         result: torch.Tensor | None = None) -> torch.Tensor:
+    """Kernel K4: reduce T outputs of each substream in-kernel; returns the
+    48-byte slp_checksum as a uint8 CUDA tensor (no host synchronisation)."""
+    gid = native_id(spec)
+    ld = states.shape[1]
+    n = ld if nstreams is None else int(nstreams)
+    if states.dtype != _word_dtype(spec.kind.w) or not states.is_cuda or states.shape[0] != spec.kind.k:
+        raise ValueError("bad states tensor")
+    dev = states.device
+    ws = _workspace(gid, dev)
+    if result is None:
+        result = torch.empty(_native.CHECKSUM_BYTES, dtype=torch.uint8, device=dev)
+    flags = _native.FUSE_INT | (_native.FUSE_F64 if f64 else 0)
+    L = _native.lib()
+    with torch.cuda.device(dev):
+        rc = L.slp_fused(gid, ctypes.c_void_p(states.data_ptr()),
+                         ctypes.c_void_p(states.data_ptr() if advance else None), ld, n, T, flags,
+                         ctypes.c_void_p(result.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                         _stream_ptr(dev))
+    _native.check(rc, "fused")
+    return result
+
+
+def decode_checksum(raw: torch.Tensor | bytes, w: int, f64: bool) -> Checksum:
+    b = bytes(raw.cpu().numpy().tobytes()) if isinstance(raw, torch.Tensor) else bytes(raw)
+    return Checksum.from_raw(_native.Checksum.from_buffer_copy(b), w, f64)
+
+
+def fused_checksum(spec: GeneratorSpec, states: torch.Tensor, T: int, *, f64: bool = False,
+                   nstreams: int | None = None, advance: bool = True) -> Checksum:
+    raw = fused_checksum_async(spec, states, T, f64=f64, nstreams=nstreams, advance=advance)
+    return decode_checksum(raw, spec.kind.w, f64)
+
+
+class Substreams:
+    """States of ``blocks x n`` substreams of one generator, resident on a GPU."""
+
+    def __init__(self, spec: GeneratorSpec, states: torch.Tensor, n: int, blocks: int = 1):
+        self.spec = spec
+        self.states = states
+        self.n = n
+        self.blocks = blocks
+        self.gid = native_id(spec)
+
+    @property
+    def count(self) -> int:
+        return self.n * self.blocks
+
+    @property
+    def device(self) -> torch.device:
+        return self.states.device
+
+    @classmethod
+    def from_generator(cls, generator: Generator, n: int, *, stride: int | None = None, blocks: int = 1,
+                       block_stride: int | None = None, first_block: int = 0, device=None) -> "Substreams":
+        """Substream i of block b = generator jumped by
+        (first_block + b) * block_stride + i * stride  (kernel K1)."""
+        spec = generator.spec
+        gid = native_id(spec)
+        dev = require_cuda(device)
+        nbits = spec.kind.n
+        stride = (1 << (nbits // 2)) if stride is None else int(stride)
+        block_stride = (1 << (3 * nbits // 4)) if block_stride is None else int(block_stride)
+        if n < 1 or blocks < 1 or stride < 0 or block_stride < 0:
+            raise ValueError("bad substream geometry")
+        k = spec.kind.k
+        bases = []
+        for b in range(first_block, first_block + blocks):
+            g = generator.clone()
+            off = b * block_stride
+            if off:
+                g.jump(compute_jump_poly(spec, off))
+            bases.extend(g.flat_words())
+        base = (ctypes.c_uint64 * len(bases))(*bases)
+        sw, sn = _native.int_to_words(stride)
+        states = torch.empty((k, n * blocks), dtype=_word_dtype(spec.kind.w), device=dev)
+        with torch.cuda.device(dev):
+            rc = _native.lib().slp_init_substreams(gid, base, blocks, sw, sn, ctypes.c_void_p(states.data_ptr()),
+                                                   n * blocks, n, _stream_ptr(dev))
+        _native.check(rc, "init_substreams")
+        return cls(spec, states, n, blocks)
+
+    @classmethod
+    def from_seed(cls, spec: GeneratorSpec, seed: int, n: int, **kw) -> "Substreams":
+        return cls.from_generator(Generator.from_seed(spec, seed), n, **kw)
+
+    @classmethod
+    def from_states(cls, spec: GeneratorSpec, flat: np.ndarray, device=None) -> "Substreams":
+        """Upload explicit flat states, a (k, L) integer array."""
+        dev = require_cuda(device)
+        flat = np.asarray(flat)
+        if flat.ndim != 2 or flat.shape[0] != spec.kind.k:
+            raise ValueError("flat states must have shape (k, L)")
+        npdt = np.uint64 if spec.kind.w == 64 else np.uint32
+        t = torch.from_numpy(np.ascontiguousarray(flat.astype(npdt))).to(dev)
+        return cls(spec, t, flat.shape[1], 1)
+
+    def states_numpy(self) -> np.ndarray:
+        return self.states.cpu().numpy()
+
+    def fill(self, T: int, *, out=None, kind: str = "native", layout: str = "stream", advance: bool = True):
+        return fill(self.spec, self.states, T, out=out, kind=kind, layout=layout, advance=advance)
+
+    def checksum(self, T: int, *, f64: bool = False, advance: bool = True) -> Checksum:
+        return fused_checksum(self.spec, self.states, T, f64=f64, advance=advance)
+
+    def checksum_async(self, T: int, *, f64: bool = False, advance: bool = True, result=None) -> torch.Tensor:
+        return fused_checksum_async(self.spec, self.states, T, f64=f64, advance=advance, result=result)
+
+    def jump(self, jp: JumpPolynomial) -> "Substreams":
+        """Advance every substream by jp.step_count steps (kernel K1, in place)."""
+        if jp.engine_key != self.spec.engine_key:
+            raise ValueError("jump polynomial was built for a different engine")
+        if jp.poly.bits == 0:
+            raise ValueError("jump polynomial is zero")
+        pw, pn = _native.int_to_words(jp.poly.bits)
+        ptr = ctypes.c_void_p(self.states.data_ptr())
+        with torch.cuda.device(self.device):
+            rc = _native.lib().slp_jump_states(self.gid, pw, pn, ptr, self.count, ptr, self.count, self.count,
+                                               _stream_ptr(self.device))
+        _native.check(rc, "jump_states")
+        return self

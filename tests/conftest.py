@@ -1,0 +1,30 @@
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) device")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+_cache = {}
+
+
+def golden(name):
+    if name not in _cache:
+        with open(os.path.join(GOLDEN, name + ".json")) as f:
+            _cache[name] = json.load(f)
+    return _cache[name]
+
+
+@pytest.fixture(scope="session")
+def G():
+    return golden

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Bit-exact for all integer and converted-float
+outputs; float64 in-kernel sums within 1e-12 relative (north_star)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1805_01407_b200 as P
+from paper_1805_01407_b200 import device as D
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ALL = P.registry_names(include_analysis=True)
+
+
+def hexs(vals):
+    return [hex(int(v)) for v in vals]
+
+
+def flat_np(name, states):
+    return states.cpu().numpy().astype(np.uint64)
+
+
+@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro128plus", "xoroshiro128plusplus",
+                                  "xoshiro512starstar", "xoroshiro1024starstar", "xoshiro128starstar",
+                                  "xoroshiro64star"])
+def test_init_substreams_dense(G, name):
+    d = G("substreams")[name]
+    sub = D.Substreams.from_seed(P.get_spec(name), d["seed"], 64)
+    S = flat_np(name, sub.states)
+    for i in range(64):
+        assert hexs(S[:, i]) == d["dense_states"][i], i
+
+
+@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro128plus", "xoshiro128starstar",
+                                  "xoroshiro64star", "xoshiro512starstar"])
+def test_init_substreams_sparse(G, name):
+    d = G("substreams")[name]
+    spec = P.get_spec(name)
+    n = (1 << 20) if spec.kind.w == 64 else (1 << 22)
+    sub = D.Substreams.from_seed(spec, d["seed"], n)
+    S = sub.states
+    for idx, want in d["sparse_states"].items():
+        i = int(idx)
+        if i < n:
+            assert hexs(S[:, i].cpu().numpy()) == want, idx
+
+
+@pytest.mark.parametrize("name", ["xoshiro512starstar", "xoroshiro1024starstar", "xoshiro256starstar"])
+def test_long_jump_blocks(G, name):
+    d = G("substreams")[name]
+    spec = P.get_spec(name)
+    sub = D.Substreams.from_seed(spec, d["seed"], 3, blocks=8)
+    S = flat_np(name, sub.states)
+    for b in range(1, 8):
+        assert hexs(S[:, b * 3]) == d["long_jump_blocks"][str(b)]
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_fill_stream_major_matches_scalar(G, name):
+    """Stream 0 = Generator.from_seed(42); stream 1 = jumped once (generators.py:315-334)."""
+    spec = P.get_spec(name)
+    d = G("generators")[name]
+    sub = D.Substreams.from_seed(spec, 42, 37)
+    out = sub.fill(100)
+    assert hexs(out[0].cpu().numpy()) == d["first_outputs_seed42"]
+    assert hexs(sub.states[:, 0].cpu().numpy()) == d["state_after_100_seed42"]
+    want_j = d["jump_outputs_seed42"][:32]
+    out2 = D.Substreams.from_seed(spec, 42, 2).fill(32)
+    assert hexs(out2[1].cpu().numpy()) == want_j
+
+
+@pytest.mark.parametrize("name", ALL)
+@pytest.mark.parametrize("T", [1, 15, 16, 33, 257, 1024])
+def test_fill_vs_oracle_ragged(name, T):
+    """Every substream, ragged stream count and lengths (tails, partial TMA boxes)."""
+    spec = P.get_spec(name)
+    rng = np.random.default_rng(T)
+    L = 45
+    k, w = spec.kind.k, spec.kind.w
+    flat = rng.integers(0, 1 << 63, size=(k, L), dtype=np.uint64) | np.uint64(1)
+    if w == 32:
+        flat &= np.uint64(0xFFFFFFFF)
+    want, want_S = O.vec_outputs(name, flat, T)
+    sub = D.Substreams.from_states(spec, flat)
+    got = sub.fill(T).cpu().numpy().astype(np.uint64)
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(flat_np(name, sub.states), want_S)
+    # position-major layout is the transpose
+    sub2 = D.Substreams.from_states(spec, flat)
+    gotp = sub2.fill(T, layout="position").cpu().numpy().astype(np.uint64)
+    np.testing.assert_array_equal(gotp, want.T)
+
+
+@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro128plus", "xoroshiro1024plusplus",
+                                  "xoshiro512plus"])
+def test_f64_bit_exact(name):
+    spec = P.get_spec(name)
+    sub = D.Substreams.from_seed(spec, 42, 100)
+    ints = D.Substreams.from_seed(spec, 42, 100).fill(300).cpu().numpy()
+    f = sub.fill(300, kind="f64").cpu().numpy()
+    np.testing.assert_array_equal(f.view(np.uint64), O.to_f64(ints).view(np.uint64))
+    assert f.min() >= 0.0 and f.max() < 1.0
+
+
+def test_f64_matches_next_double(G):
+    spec = P.get_spec("xoshiro256starstar")
+    f = D.Substreams.from_seed(spec, 42, 1).fill(16, kind="f64").cpu().numpy()[0]
+    assert [float.hex(float(x)) for x in f] == G("generators")["xoshiro256starstar"]["first_doubles_seed42"]
+
+
+@pytest.mark.parametrize("name", ["xoshiro128starstar", "xoshiro128plusplus", "xoroshiro64star",
+                                  "xoroshiro64starstar"])
+def test_f32_and_u64_kinds(name):
+    spec = P.get_spec(name)
+    ints = D.Substreams.from_seed(spec, 7, 70).fill(200).cpu().numpy()
+    f = D.Substreams.from_seed(spec, 7, 70).fill(200, kind="f32").cpu().numpy()
+    np.testing.assert_array_equal(f.view(np.uint32), O.to_f32(ints).view(np.uint32))
+    u = D.Substreams.from_seed(spec, 7, 70).fill(200, kind="u64").cpu().numpy()
+    np.testing.assert_array_equal(u, ints.astype(np.uint64))
+    with pytest.raises(ValueError):
+        D.Substreams.from_seed(spec, 7, 4).fill(8, kind="f64")
+
+
+def test_unaligned_pitch_uses_staged_path():
+    spec = P.get_spec("xoshiro256plusplus")
+    flat_sub = D.Substreams.from_seed(spec, 42, 50)
+    ref = D.Substreams.from_seed(spec, 42, 50).fill(130).cpu().numpy()
+    big = torch.zeros((50, 133), dtype=torch.uint64, device="cuda")
+    view = big[:, 1:131]  # row pitch 133 elements, base not 16-byte aligned
+    D.fill(spec, flat_sub.states, 130, out=view)
+    np.testing.assert_array_equal(view.cpu().numpy(), ref)
+    assert int(big[:, 0].cpu().numpy().max()) == 0 and int(big[:, 131:].cpu().numpy().max()) == 0
+
+
+@pytest.mark.parametrize("key", ["c2s/xoshiro256plus", "c2s/xoshiro256plusplus", "c2s/xoshiro256starstar",
+                                 "c3s/xoroshiro128plus", "c3s/xoroshiro128plusplus", "c3s/xoroshiro128starstar",
+                                 "c4s/xoshiro128starstar", "c4s/xoshiro128plusplus", "c4s/xoroshiro64star",
+                                 "c4s/xoroshiro64starstar", "c5s/xoshiro512starstar", "c5s/xoshiro512plusplus",
+                                 "c5s/xoroshiro1024starstar", "c5s/xoroshiro1024plusplus"])
+def test_fused_small_configs(G, key):
+    g = G("checksums_small")[key]
+    spec = P.get_spec(g["name"])
+    sub = D.Substreams.from_seed(spec, g["seed"], g["substreams"], blocks=g["blocks"])
+    c = sub.checksum(g["T"], f64=True)
+    assert hex(c.sum) == g["sum"] and hex(c.xor) == g["xor"] and hex(c.mant) == g["mant"]
+    assert float.hex(c.fsum) == g["fsum"]
+    assert abs(c.fsum_f64 - c.fsum) <= 1e-12 * abs(c.fsum)
+    assert c.count == g["blocks"] * g["substreams"] * g["T"]
+
+
+@pytest.mark.parametrize("key", ["c2/xoshiro256plus", "c2/xoshiro256plusplus", "c2/xoshiro256starstar",
+                                 "c3/xoroshiro128plus", "c3/xoroshiro128plusplus", "c3/xoroshiro128starstar",
+                                 "c4/xoshiro128starstar", "c4/xoshiro128plusplus", "c4/xoroshiro64star",
+                                 "c4/xoroshiro64starstar", "c5/xoshiro512starstar", "c5/xoshiro512plusplus",
+                                 "c5/xoroshiro1024starstar", "c5/xoroshiro1024plusplus"])
+def test_fused_full_size_configs(G, key):
+    """BASELINE configs 2-5 at full size: checksums equal the reference's."""
+    g = G("checksums_big").get(key)
+    if g is None:
+        pytest.skip("golden checksum not generated")
+    spec = P.get_spec(g["name"])
+    sub = D.Substreams.from_seed(spec, g["seed"], g["substreams"], blocks=g["blocks"])
+    c = sub.checksum(g["T"], f64=True)
+    assert hex(c.sum) == g["sum"] and hex(c.xor) == g["xor"] and hex(c.mant) == g["mant"]
+    assert float.hex(c.fsum) == g["fsum"]
+    assert abs(c.fsum_f64 - c.fsum) <= 1e-12 * abs(c.fsum)
+
+
+def test_store_equals_fused_full_config2(G):
+    """Config 2 store mode (8 GiB): the stored outputs reduce to the reference checksum."""
+    g = G("checksums_big").get("c2/xoshiro256starstar")
+    if g is None:
+        pytest.skip("golden checksum not generated")
+    spec = P.get_spec("xoshiro256starstar")
+    sub = D.Substreams.from_seed(spec, 42, 1 << 20)
+    out = sub.fill(1024)
+    v = out.view(torch.int64)
+    s = int(v.sum(dtype=torch.int64).item()) & ((1 << 64) - 1)  # wraps mod 2^64
+    x = v[:, 0].clone()
+    cols = v
+    while cols.shape[1] > 1:
+        h = cols.shape[1] // 2
+        cols = cols[:, :h] ^ cols[:, h:2 * h]
+    xr = cols[:, 0]
+    while xr.numel() > 1:
+        h = xr.numel() // 2
+        xr = xr[:h] ^ xr[h:2 * h]
+    del x
+    assert hex(s) == g["sum"]
+    assert hex(int(xr.item()) & ((1 << 64) - 1)) == g["xor"]
+
+
+@pytest.mark.parametrize("key", ["xoroshiro128plus/5/2500/6/128", "xoshiro256starstar/5/2500/6/128",
+                                 "xoroshiro1024plusplus/5/2500/6/128", "xorshift128/5/2500/6/128",
+                                 "xoshiro128plus/5/2500/6/128", "xoshiro256plus/8/700/1/256",
+                                 "xoshiro256starstar/42/5000/4/1000", "xoroshiro64starstar/3/3000/5/256",
+                                 "xoshiro512plusplus/11/4096/8/128"])
+def test_output_stream_matches_reference(G, key):
+    d = G("laned")[key]
+    spec = P.get_spec(d["name"])
+    chunks = list(P.output_stream(spec, seed=d["seed"], total_values=d["total"], lanes=d["lanes"],
+                                  lane_len=d["lane_len"]))
+    assert [c.size for c in chunks] == d["chunk_sizes"]
+    assert all(c.dtype == np.uint64 for c in chunks)
+    assert hexs(np.concatenate(chunks)) == d["values"]
+
+
+def test_output_stream_config1(G):
+    """Config 1: xoshiro256** seed 42, 2^20 outputs through the laned bulk API."""
+    spec = P.get_spec("xoshiro256starstar")
+    vals = np.concatenate(list(P.output_stream(spec, seed=42, total_values=1 << 20)))
+    assert vals.size == 1 << 20
+    assert hex(int(vals[0])) == "0x15780b2e0c2ec716"
+    assert hex(int(vals[-1])) == "0x6569564c7df21f30"
+    c = O.checksum(vals, 64)
+    assert hex(c["sum"]) == "0x89f6597c294a86e6" and hex(c["xor"]) == "0x40c711d84f637bcc"
+
+
+def test_jump_states_matches_host(G):
+    spec = P.get_spec("xoroshiro1024plusplus")
+    sub = D.Substreams.from_seed(spec, 42, 9)
+    before = flat_np("x", sub.states)
+    jp = P.compute_jump_poly(spec, 123456789)
+    sub.jump(jp)
+    after = flat_np("x", sub.states)
+    for i in range(9):
+        g = P.Generator(spec, [int(v) for v in before[:, i]], ptr=spec.kind.k - 1)
+        g.jump(jp)
+        assert list(g.flat_words()) == [int(v) for v in after[:, i]]
+
+
+def test_errors():
+    spec = P.get_spec("xoshiro256plus")
+    with pytest.raises(ValueError):
+        D.Substreams.from_seed(P.custom_spec("xoroshiro", 2, 5, 1, 3, 1), 1, 4)
+    sub = D.Substreams.from_seed(spec, 1, 4)
+    with pytest.raises(ValueError):
+        sub.jump(P.compute_jump_poly(P.get_spec("xoroshiro128"), 5))
+    with pytest.raises(ValueError):
+        sub.fill(4, kind="f32")
