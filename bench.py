@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Headline benchmark: BASELINE.json config 2 with xoshiro256** —
+2^20 substreams (stream i = seed 42 jumped i * 2^128), 1024 uint64 outputs
+each, stored stream-major to HBM (8 GiB per step) by kernel K2 (TMA stores).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the hot path over the batch: every substream emits its
+next 1024 outputs (states resident in HBM, advanced in place).  The output
+(8 GiB) is far larger than L2 (126 MB), so no L2 flush is needed between
+steps.  Multi-GPU (torchrun): rank r generates long-jump block r (substreams
+seed * M^(r*2^192 + i*2^128)); there is no data-path collective (weak scaling);
+timing is the max over ranks of CUDA-event time.  ``--impl reference`` times
+the reference's CPU algorithm (oracle/cpu_baseline.py, numpy port, all host
+cores) on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GEN = "xoshiro256starstar"
+SEED = 42
+N_STREAMS = 1 << 20
+T = 1024
+METRIC = "xoshiro256** 64-bit outputs/s"
+UNIT = "outputs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--extra", action="store_true", help="also time fused mode and substream init")
+    return ap.parse_args()
+
+
+def config(world):
+    return {"workload": "BASELINE config 2: xoshiro256** 2^20 substreams x 1024 u64, store mode (8 GiB/step/GPU)",
+            "generator": GEN, "seed": SEED, "substreams_per_gpu": N_STREAMS, "outputs_per_substream": T,
+            "layout": "stream-major [substream][position]", "store_path": "TMA bulk tensor store (K2)",
+            "l2": "output 8 GiB/step >> 126 MB L2; no flush needed",
+            "partition": "rank r = long-jump block r (seed*M^(r*2^192))", "world_size": world}
+
+
+# ---------------------------------------------------------------- clocks (NVML)
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons every 10 ms in a thread."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index):
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self.samples = []
+        self.reasons = 0
+        self._stop = threading.Event()
+
+    def sample(self):
+        if not self.ok:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(0.01)
+
+    def start(self):
+        self.samples, self.reasons = [], 0
+        self._stop.clear()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        self._stop.set()
+        self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [k for k, v in self.REASONS.items() if self.reasons & v and k != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- helpers
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def ncu_traffic(kernel_tag):
+    """dram read+write bytes per launch of the fill kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(kernel_tag, {}).get("dram_bytes_per_launch")
+    except OSError:
+        return None
+
+
+def cpu_baseline(steps_budget_s=20.0):
+    from oracle.cpu_baseline import CpuBaseline
+
+    cb = CpuBaseline(GEN, SEED, T)
+    try:
+        lanes = cb.calibrate(min(4.0, steps_budget_s / 4))
+        tot, secs = 0, 0.0
+        reps = 0
+        while secs < steps_budget_s / 2 and reps < 8:
+            n, dt = cb.step(lanes)
+            tot += n
+            secs += dt
+            reps += 1
+        return {"value": tot / secs, "unit": UNIT, "cores": cb.procs, "kind": "port",
+                "sample": f"{reps} x ({cb.procs} procs x {lanes} substreams x {T} outputs) of config 2, "
+                          "numpy port of LanedStream lane set-up + VecStepper/apply_vec (oracle/cpu_baseline.py), "
+                          "lane set-up included"}
+    finally:
+        cb.close()
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1805_01407_b200 as P
+    from paper_1805_01407_b200 import device as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    spec = P.get_spec(GEN)
+    k = spec.kind.k
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # substream init (K1), timed separately (setup; not in the step)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    D.Substreams.from_seed(spec, SEED, N_STREAMS, first_block=rank)  # plan + poly upload (host, once)
+    torch.cuda.synchronize()
+    t0.record()
+    sub = D.Substreams.from_seed(spec, SEED, N_STREAMS, first_block=rank)
+    t1.record()
+    torch.cuda.synchronize()
+    init_ms = t0.elapsed_time(t1)
+
+    out = torch.empty((N_STREAMS, T), dtype=torch.uint64, device=dev)
+    for _ in range(args.warmup):
+        sub.fill(T, out=out)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(args.steps):
+        sub.fill(T, out=out)
+    end.record()
+    clocks.sample()
+    torch.cuda.synchronize()
+    clocks.stop()
+    barrier()
+    torch.cuda.synchronize()
+    ms_local = start.elapsed_time(end)
+    ms = max_over_ranks(ms_local)
+    outputs_per_step = N_STREAMS * T * world
+    value = outputs_per_step * args.steps / (ms / 1e3)
+
+    # roofline of the dominant (only) kernel of the step: k_fill<xoshiro256**, native, TMA>
+    launch_ms = ms_local / args.steps
+    alg_bytes = N_STREAMS * T * 8 + 2 * N_STREAMS * k * 8
+    peaks, src = measured_peaks()
+    achieved = alg_bytes / (launch_ms / 1e3) / 1e9
+    traffic = ncu_traffic("k_fill_xoshiro256starstar_u64_tma")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+                "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs: copy read+write, burst)",
+                "alg_bytes_per_launch": alg_bytes,
+                "alg_bytes_per_unit": "8 B per u64 output + 64 B state read/write per substream per launch",
+                "kernel": "k_fill<xoshiro256**, u64, TMA>", "launch_ms": round(launch_ms, 4),
+                "frac_of_8TBps_spec": round(achieved / 8000.0, 4)}
+
+    # e2e: public API from the seed to HOST memory, every step: substream init
+    # (H2D: the base state, k words) + fill + D2H of all outputs (pinned), overlapped
+    e2e = None
+    if args.e2e_steps > 0:
+        host = torch.empty((N_STREAMS, T), dtype=torch.uint64, pin_memory=True)
+        bufs = [torch.empty((1 << 17, T), dtype=torch.uint64, device=dev) for _ in range(2)]
+        del out
+        for i in range(args.e2e_steps + 1):
+            if i == 1:
+                barrier()
+                torch.cuda.synchronize()
+                t_start = time.perf_counter()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            s2 = D.Substreams.from_seed(spec, SEED, N_STREAMS, first_block=rank)
+            D.fill_to_host(spec, s2.states, T, host, _bufs=bufs)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(e0.elapsed_time(e1))
+        wall = time.perf_counter() - t_start
+        e2e = {"value": outputs_per_step * args.e2e_steps / (e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": k * 8, "d2h_bytes_per_step": N_STREAMS * T * 8,
+               "api": "Substreams.from_seed + device.fill_to_host (pinned host, D2H overlapped)",
+               "ms_per_step": round(e_ms / args.e2e_steps, 3), "wall_s": round(wall, 3)}
+        del host, bufs
+
+    extra = {}
+    if args.extra:
+        extra = run_extra(spec, dev, rank)
+
+    if rank == 0:
+        cb = None
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_baseline()
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, SplitMix64)",
+                "config": config(world), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+                "clocks": clocks.summary(), "gpu_launches": args.steps,
+                "init_ms_2^20_substreams": round(init_ms, 3)}
+        line.update(extra)
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_extra(spec, dev, rank):
+    """Fused mode (K4) on the same substreams + init cost, for DESIGN.md."""
+    import torch
+
+    from paper_1805_01407_b200 import device as D
+
+    res = {}
+    sub = D.Substreams.from_seed(spec, SEED, N_STREAMS, first_block=rank)
+    raw = torch.empty(48, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        sub.checksum_async(T, result=raw)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 50
+    e0.record()
+    for _ in range(reps):
+        sub.checksum_async(T, result=raw)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    res["fused_int"] = {"outputs_per_s": N_STREAMS * T / (ms / 1e3), "ms_per_step": ms}
+    e0.record()
+    for _ in range(reps):
+        sub.checksum_async(T, f64=True, result=raw)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    res["fused_int_f64"] = {"outputs_per_s": N_STREAMS * T / (ms / 1e3), "ms_per_step": ms}
+    out = torch.empty((N_STREAMS, T), dtype=torch.float64, device=dev)
+    sub.fill(T, out=out, kind="f64")
+    e0.record()
+    for _ in range(20):
+        sub.fill(T, out=out, kind="f64")
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    res["store_f64"] = {"outputs_per_s": N_STREAMS * T / (ms / 1e3), "ms_per_step": ms}
+    return {"extra": res}
+
+
+# ---------------------------------------------------------------- reference arm
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.cpu_baseline import CpuBaseline
+
+    budget = 120.0
+    per_step = max(0.05, min(3.0, budget / max(1, args.steps + args.warmup)))
+    cb = CpuBaseline(GEN, SEED, T)
+    try:
+        lanes = cb.calibrate(per_step)
+        for _ in range(args.warmup):
+            cb.step(lanes)
+        tot, secs = 0, 0.0
+        for _ in range(args.steps):
+            n, dt = cb.step(lanes)
+            tot += n
+            secs += dt
+    finally:
+        cb.close()
+    value = tot / secs
+    sample = (f"each step: {cb.procs} procs x {lanes} substreams x {T} outputs of config 2 "
+              "(numpy port of the reference's LanedStream lane set-up + VecStepper/apply_vec)")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded, SplitMix64)", "config": config(world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb.procs, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -55,8 +55,9 @@ typedef enum slp_layout {
 
 /* Consumer flags for slp_fused. */
 typedef enum slp_fuse_flags {
-  SLP_FUSE_INT = 1, /* wrapping sum, xor, exact sum of x and of the low bits        */
-  SLP_FUSE_F64 = 2  /* additionally a real float64 accumulation of the converted values */
+  SLP_FUSE_INT = 1,   /* wrapping sum mod 2^64 and xor of all outputs                    */
+  SLP_FUSE_F64 = 2,   /* + a float64 accumulation of the converted values (implies EXACT) */
+  SLP_FUSE_EXACT = 4  /* + exact 128-bit sum and low-bit sum: exact float sum (mant)      */
 } slp_fuse_flags;
 
 typedef struct slp_gen_info {
@@ -67,9 +68,11 @@ typedef struct slp_gen_info {
 } slp_gen_info;
 
 /* Result of the fused consumer.  All integer fields are exact and independent
- * of summation order; `mant` = (sum - low_sum) >> shift is the exact integer
- * sum of (x >> shift), shift = 11 (w=64) or 8 (w=32), so the float64 sum of
- * the converted values is mant * 2^-(53|24) rounded once. */
+ * of summation order.  With SLP_FUSE_EXACT (or F64), sum_hi:sum_lo is the
+ * exact sum and mant = (sum - low_sum) >> shift is the exact integer sum of
+ * (x >> shift), shift = 11 (w=64) or 8 (w=32), so the float64 sum of the
+ * converted values is mant * 2^-(53|24) rounded once.  Without it only sum_lo
+ * (the wrapping checksum) and xor_all are defined. */
 typedef struct slp_checksum {
   uint64_t sum_lo;  /* sum of outputs mod 2^64 (the wrapping checksum)          */
   uint64_t sum_hi;  /* bits 64..127 of the exact sum of outputs                  */

@@ -26,7 +26,7 @@ SLP_ERR_BUFFER = -7
 
 OUT_NATIVE, OUT_U64, OUT_F64, OUT_F32 = 0, 1, 2, 3
 STREAM_MAJOR, POSITION_MAJOR = 0, 1
-FUSE_INT, FUSE_F64 = 1, 2
+FUSE_INT, FUSE_F64, FUSE_EXACT = 1, 2, 4
 
 u64p = ctypes.POINTER(ctypes.c_uint64)
 vp = ctypes.c_void_p

@@ -84,8 +84,8 @@ int check_launch(const char *what) {
 bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out) {
   static int path = env_int("SLP_STORE_PATH", 0);
   if (path == 2) return false;
-  const uint64_t ch = 128 / es;
-  return ((uintptr_t)out % 16) == 0 && (ld_out * es) % 16 == 0 && T >= ch && T < (1ull << 31) &&
+  const uint64_t seg = 128 / es;  // elements per 128-byte segment
+  return ((uintptr_t)out % 128) == 0 && (ld_out * es) % 16 == 0 && T >= kSegs * seg && T < (1ull << 40) &&
          nstreams < (1ull << 31) && ld_out * es < (1ull << 40) && ld_out >= T;
 }
 
@@ -102,17 +102,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// Stream-major output [nstreams][ld_out] viewed as a 3-D tensor
+// (element within a 128-byte segment, substream, segment index) so that one
+// box {128/es, 32, kSegs} is 32 substreams x kSegs contiguous segments.
 int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out) {
   auto fn = encode_fn();
   if (!fn) {
     set_last_error("cuTensorMapEncodeTiled unavailable");
     return SLP_ERR_CUDA;
   }
-  cuuint64_t gdim[2] = {(cuuint64_t)T, (cuuint64_t)nstreams};
-  cuuint64_t gstride[1] = {(cuuint64_t)(ld_out * es)};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / es), 32};
-  cuuint32_t estride[2] = {1, 1};
-  CUresult r = fn(map, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, gdim,
+  const uint64_t seg = 128 / es;
+  cuuint64_t gdim[3] = {(cuuint64_t)seg, (cuuint64_t)nstreams, (cuuint64_t)(T / seg)};
+  cuuint64_t gstride[2] = {(cuuint64_t)(ld_out * es), 128};
+  cuuint32_t box[3] = {(cuuint32_t)seg, 32, (cuuint32_t)kSegs};
+  cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = fn(map, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, out, gdim,
                   gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -360,7 +364,7 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
   if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
   const GenOps *ops = gen_ops(id);
   if (!ops) return SLP_ERR_UNSUPPORTED;
-  if (!states_in || !result || !workspace || ld < nstreams || !(flags & (SLP_FUSE_INT | SLP_FUSE_F64)))
+  if (!states_in || !result || !workspace || ld < nstreams || !(flags & (SLP_FUSE_INT | SLP_FUSE_F64 | SLP_FUSE_EXACT)))
     return SLP_ERR_INVALID;
   FusedParams p{};
   p.sin = states_in;

@@ -35,17 +35,82 @@ struct WordOf<32> {
   using type = uint32_t;
 };
 
+// Word operations.  64-bit words are manipulated as explicit 32-bit halves:
+// rotations are two funnel shifts (SHF.L.W), constant shifts one funnel shift
+// plus one plain shift, and multiplication by a constant C < 2^32 is one
+// IMAD.WIDE.U32 plus one IMAD (three for a 64-bit constant), which is what
+// the SASS count per output is built on.
+template <int W>
+struct WOps;
+
+template <>
+struct WOps<32> {
+  using word = uint32_t;
+  template <int R>
+  static __device__ __forceinline__ word rotl(word x) {
+    return __funnelshift_l(x, x, R);
+  }
+  template <int B>
+  static __device__ __forceinline__ word shl(word x) {
+    return x << B;
+  }
+  template <int B>
+  static __device__ __forceinline__ word shr(word x) {
+    return x >> B;
+  }
+  template <unsigned long long C>
+  static __device__ __forceinline__ word mulc(word x) {
+    return x * (uint32_t)C;
+  }
+};
+
+template <>
+struct WOps<64> {
+  using word = uint64_t;
+  static __device__ __forceinline__ uint32_t lo(word x) { return (uint32_t)x; }
+  static __device__ __forceinline__ uint32_t hi(word x) { return (uint32_t)(x >> 32); }
+  static __device__ __forceinline__ word pack(uint32_t l, uint32_t h) { return ((uint64_t)h << 32) | l; }
+  template <int R>
+  static __device__ __forceinline__ word rotl(word x) {
+    uint32_t l = lo(x), h = hi(x);
+    if constexpr (R >= 32) {
+      const uint32_t t = l;
+      l = h;
+      h = t;
+    }
+    constexpr int r = R & 31;
+    if constexpr (r == 0) return pack(l, h);
+    return pack(__funnelshift_l(h, l, r), __funnelshift_l(l, h, r));
+  }
+  template <int B>
+  static __device__ __forceinline__ word shl(word x) {
+    if constexpr (B >= 32) return pack(0u, lo(x) << (B - 32));
+    return pack(lo(x) << B, __funnelshift_l(lo(x), hi(x), B));
+  }
+  template <int B>
+  static __device__ __forceinline__ word shr(word x) {
+    if constexpr (B >= 32) return pack(hi(x) >> (B - 32), 0u);
+    return pack(__funnelshift_r(lo(x), hi(x), B), hi(x) >> B);
+  }
+  template <unsigned long long C>
+  static __device__ __forceinline__ word mulc(word x) {
+    const uint64_t p = (uint64_t)lo(x) * (uint32_t)C;  // IMAD.WIDE.U32
+    uint32_t h = hi(x) * (uint32_t)C + (uint32_t)(p >> 32);
+    if constexpr ((C >> 32) != 0) h += lo(x) * (uint32_t)(C >> 32);
+    return pack((uint32_t)p, h);
+  }
+};
+
 template <int FAM, int K, int W, int A, int B, int C, int SC, int WI, int WJ, unsigned long long S_, int R_,
           unsigned long long T_>
 struct Gen {
   using word = typename WordOf<W>::type;
+  using O = WOps<W>;
   static constexpr int k = K;
   static constexpr int w = W;
   static constexpr int n = K * W;
   static constexpr int pw = n / 64;  // u64 words per jump polynomial (degree < n)
   static constexpr bool ring = FAM != SLP_FAM_XOSHIRO;
-
-  static __device__ __forceinline__ word rotl(word x, int r) { return (word)((x << r) | (x >> (W - r))); }
 
   // register slot of flat word j when the ring offset is o (constant after unrolling)
   static __device__ __forceinline__ constexpr int slot(int o, int j) { return ring ? (o + j) % K : j; }
@@ -58,11 +123,11 @@ struct Gen {
     } else if constexpr (SC == SLP_SC_PLUS) {
       return (word)(xi + s[slot(o, WJ)]);
     } else if constexpr (SC == SLP_SC_STAR) {
-      return (word)(xi * (word)S_);
+      return O::template mulc<S_>(xi);
     } else if constexpr (SC == SLP_SC_PLUSPLUS) {
-      return (word)(rotl((word)(xi + s[slot(o, WJ)]), R_) + xi);
+      return (word)(O::template rotl<R_>((word)(xi + s[slot(o, WJ)])) + xi);
     } else {
-      return (word)(rotl((word)(xi * (word)S_), R_) * (word)T_);
+      return O::template mulc<T_>(O::template rotl<R_>(O::template mulc<S_>(xi)));
     }
   }
 
@@ -73,23 +138,23 @@ struct Gen {
       const int i0 = slot(o, 0), il = slot(o, K - 1);
       const word x0 = s[i0];
       const word xl = s[il] ^ x0;
-      s[il] = rotl(x0, A) ^ xl ^ (word)(xl << B);
-      s[i0] = rotl(xl, C);
+      s[il] = O::template rotl<A>(x0) ^ xl ^ O::template shl<B>(xl);
+      s[i0] = O::template rotl<C>(xl);
     } else if constexpr (FAM == SLP_FAM_XORSHIFT) {
       const int i0 = slot(o, 0), i1 = slot(o, 1);
       const word s0 = s[i0], s1 = s[i1];
-      const word t = s0 ^ (word)(s0 << A);
-      s[i0] = t ^ (t >> B) ^ s1 ^ (s1 >> C);
+      const word t = s0 ^ O::template shl<A>(s0);
+      s[i0] = t ^ O::template shr<B>(t) ^ s1 ^ O::template shr<C>(s1);
     } else if constexpr (K == 4) {
-      const word t = (word)(s[1] << A);
+      const word t = O::template shl<A>(s[1]);
       s[2] ^= s[0];
       s[3] ^= s[1];
       s[1] ^= s[2];
       s[0] ^= s[3];
       s[2] ^= t;
-      s[3] = rotl(s[3], B);
+      s[3] = O::template rotl<B>(s[3]);
     } else {
-      const word t = (word)(s[1] << A);
+      const word t = O::template shl<A>(s[1]);
       s[2] ^= s[0];
       s[5] ^= s[1];
       s[1] ^= s[2];
@@ -99,7 +164,7 @@ struct Gen {
       s[0] ^= s[6];
       s[6] ^= s[7];
       s[6] ^= t;
-      s[7] = rotl(s[7], B);
+      s[7] = O::template rotl<B>(s[7]);
     }
   }
 
@@ -116,17 +181,6 @@ struct Gen {
     return out;
   }
 };
-
-// CH outputs; CH % K == 0 for ring engines so the ring offset returns to 0
-template <class G, int CH>
-__device__ __forceinline__ void gen_chunk(typename G::word (&s)[G::k], typename G::word (&o)[CH]) {
-  static_assert(!G::ring || CH % G::k == 0, "chunk must be a multiple of the ring size");
-#pragma unroll
-  for (int t = 0; t < CH; ++t) {
-    o[t] = G::output(s, t % G::k);
-    G::step(s, t % G::k);
-  }
-}
 
 // ---- output conversion (K3) ------------------------------------------------
 // bit patterns of the converted element; conversion is exact in both cases:
@@ -182,6 +236,16 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+// warp index the compiler can prove warp-uniform (result of a shuffle from lane 0)
+__device__ __forceinline__ int warp_uniform() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+// one elected lane of a converged warp (elect.sync picks the same leader every time)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 // 128-bit accumulate of a 64-bit value
 __device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t x) {
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(lo), "+l"(hi) : "l"(x));
@@ -190,115 +254,151 @@ __device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t x) {
 // ---- K2/K3: fill ---------------------------------------------------------------
 //
 // A warp owns 32 consecutive substreams ("unit"); lane l keeps substream
-// u*32+l in registers and emits 128 B (CH outputs) per chunk.  MODE:
-//   FILL_TMA     stream-major; the warp's 32 x 128 B tile is staged in shared
-//                memory with the 128B swizzle (conflict-free STS.128) and
-//                written by one TMA bulk tensor store (cp.async.bulk.tensor),
-//                double-buffered so generation overlaps the store;
-//   FILL_STAGED  stream-major, same staging, element stores (any alignment);
-//   FILL_POS     position-major: each step is one coalesced warp store.
+// u*32+l in registers.  Outputs are produced in tiles of 32 substreams x
+// kTileRowBytes (= kSegs x 128 B) per substream; CH = kTileRowBytes / ES
+// outputs per substream per tile.  MODE:
+//   FILL_TMA     stream-major.  Every output pair goes to the warp's
+//                shared-memory tile as it is produced (STS.128,
+//                conflict-free under the 128B swizzle), and the full tile
+//                leaves with one 3-D TMA bulk tensor store
+//                (cp.async.bulk.tensor.3d, SASS UTMASTG) that writes
+//                kTileRowBytes contiguous bytes of each of the 32 rows.  The
+//                row piece is >= 256 B because HBM absorbs a column sweep of
+//                64/128-byte pieces at only ~4.5-4.8 TB/s (profiles/wpattern.cu).
+//                Two buffers per warp: store i-2 must have finished reading
+//                before tile i overwrites its buffer (cp.async.bulk.wait_group.read).
+//   FILL_STAGED  stream-major, same staging, element stores (any pitch/alignment);
+//   FILL_POS     position-major: each output is one coalesced warp store.
+// Shared-memory tile layout [seg][row][128 B], chunk q of (seg, row) at
+// ((seg*32 + row) * 128) + ((q ^ (row & 7)) << 4)  (CU_TENSOR_MAP_SWIZZLE_128B).
 
 enum { FILL_TMA = 0, FILL_STAGED = 1, FILL_POS = 2 };
-constexpr int kFillWarps = 4;
-constexpr int kFillBufs = 2;
-constexpr int kTileBytes = 32 * 128;
+constexpr int kFillThreads = kFillWarps * 32;
+constexpr int kTileRowBytes = kSegs * 128;
+constexpr int kTileBytes = 32 * kTileRowBytes;
 constexpr int kFillSmem = kFillWarps * kFillBufs * kTileBytes + 1024;
 
+__host__ __device__ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+
+__device__ __forceinline__ uint32_t swz(int seg, int r, int q) { return ((seg * 32 + r) << 7) + ((q ^ (r & 7)) << 4); }
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+               :
+               : "l"(reinterpret_cast<uint64_t>(map)), "r"(src), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
 template <class G, int OK, int MODE>
-__global__ void __launch_bounds__(kFillWarps * 32) k_fill(FillParams p, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __grid_constant__ CUtensorMap tmap) {
   using word = typename G::word;
-  using O = Out<OK, word>;
-  using bits = typename O::bits;
+  using Cv = Out<OK, word>;
+  using bits = typename Cv::bits;
   constexpr int K = G::k;
   constexpr int ES = sizeof(bits);
-  constexpr int CH = 128 / ES;   // outputs per 128-byte row
-  constexpr int EPC = 16 / ES;   // elements per 16-byte chunk
+  constexpr int CH = kTileRowBytes / ES;                          // outputs per substream per tile
+  constexpr int EPC = 16 / ES;                                    // elements per 16-byte chunk
+  static_assert(!G::ring || CH % K == 0, "tile must cover whole ring periods");
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int warp = warp_uniform();  // keeps TMA coordinates in uniform registers
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *wtiles = nullptr;
-  if constexpr (MODE != FILL_POS) {
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t aligned = (raw + 1023u) & ~1023u;  // 128B swizzle atoms are 1 KiB
-    wtiles = smem_raw + (aligned - raw) + warp * kFillBufs * kTileBytes;
-  }
+  uint32_t tiles = 0;
+  if constexpr (MODE != FILL_POS)
+    tiles = ((smem_u32(smem_raw) + 1023u) & ~1023u) + warp * kFillBufs * kTileBytes;  // 128B-swizzle atoms: 1 KiB
 
   const word *__restrict__ sin = static_cast<const word *>(p.sin);
   word *sout = static_cast<word *>(p.sout);
   bits *__restrict__ out = static_cast<bits *>(p.out);
-  const uint64_t nfull = p.T / CH;
-  const uint64_t rem = p.T - nfull * CH;
-  uint32_t issued = 0;
+  const uint64_t ntiles = p.T / CH;
+  const uint64_t rem = p.T - ntiles * CH;
+  uint32_t issued = 0;  // tiles produced by this warp
 
   for (uint64_t u = (uint64_t)blockIdx.x * kFillWarps + warp; u < p.nunits; u += (uint64_t)gridDim.x * kFillWarps) {
-    const uint64_t stream = u * 32 + lane;
+    const uint64_t row0 = u * 32;
+    const uint64_t stream = row0 + lane;
     const bool valid = stream < p.nstreams;
     word s[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) s[j] = valid ? sin[j * p.ld + stream] : (word)0;
 
-    for (uint64_t c = 0; c < nfull; ++c) {
-      word o[CH];
-      gen_chunk<G, CH>(s, o);
-      if constexpr (MODE == FILL_POS) {
-        if (valid) {
-          bits *dst = out + (c * CH) * p.ld_out + stream;
-#pragma unroll
-          for (int t = 0; t < CH; ++t) dst[(uint64_t)t * p.ld_out] = O::conv(o[t]);
-        }
-      } else {
-        uint8_t *tile = wtiles + (issued & (kFillBufs - 1)) * kTileBytes;
+    for (uint64_t c = 0; c < ntiles; ++c) {
+      const uint64_t pos0 = c * CH;
+      uint32_t tile = 0;
+      if constexpr (MODE != FILL_POS) {
+        tile = tiles + (issued & (kFillBufs - 1)) * kTileBytes;
         if constexpr (MODE == FILL_TMA) {
-          if (lane == 0 && issued >= kFillBufs) bulk_wait_read<kFillBufs - 1>();
+          if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
         }
         __syncwarp();
-        // row `lane`, 16-byte chunk q stored at chunk q ^ (lane & 7)  (CU_TENSOR_MAP_SWIZZLE_128B)
-        uint8_t *row = tile + lane * 128;
+      }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          uint8_t *dst = row + ((q ^ (lane & 7)) << 4);
-          if constexpr (ES == 8) {
-            *reinterpret_cast<ulonglong2 *>(dst) =
-                make_ulonglong2((unsigned long long)O::conv(o[2 * q]), (unsigned long long)O::conv(o[2 * q + 1]));
-          } else {
-            *reinterpret_cast<uint4 *>(dst) = make_uint4((uint32_t)O::conv(o[4 * q]), (uint32_t)O::conv(o[4 * q + 1]),
-                                                         (uint32_t)O::conv(o[4 * q + 2]), (uint32_t)O::conv(o[4 * q + 3]));
-          }
+      for (int e = 0; e < CH; e += EPC) {
+        bits v[EPC];
+#pragma unroll
+        for (int i = 0; i < EPC; ++i) {
+          const int o = (e + i) % K;
+          v[i] = Cv::conv(G::output(s, o));
+          G::step(s, o);
         }
-        if constexpr (MODE == FILL_TMA) {
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmap, smem_u32(tile), (int)(c * CH), (int)(u * 32));
-            bulk_commit();
+        if constexpr (MODE == FILL_POS) {
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < EPC; ++i) out[(pos0 + e + i) * p.ld_out + stream] = v[i];
           }
         } else {
-          __syncwarp();
-          // element stores, lanes sweep rows: ES=8 -> 2 rows per pass, ES=4 -> 1 row
-          constexpr int LPR = CH;  // lanes per row
-          constexpr int RPP = 32 / LPR;
-#pragma unroll 4
-          for (int r0 = 0; r0 < 32; r0 += RPP) {
-            const int r = r0 + lane / LPR;
-            const int e = lane % LPR;
-            const uint64_t srow = u * 32 + r;
-            const bits v = *reinterpret_cast<const bits *>(tile + r * 128 + (((e / EPC) ^ (r & 7)) << 4) + (e % EPC) * ES);
-            if (srow < p.nstreams) out[srow * p.ld_out + c * CH + e] = v;
+          const int byte = e * ES;
+          const uint32_t addr = tile + swz(byte >> 7, lane, (byte & 127) >> 4);
+          if constexpr (ES == 8) {
+            asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(addr), "l"((uint64_t)v[0]), "l"((uint64_t)v[1])
+                         : "memory");
+          } else {
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"((uint32_t)v[0]),
+                         "r"((uint32_t)v[1]), "r"((uint32_t)v[2]), "r"((uint32_t)v[3])
+                         : "memory");
           }
-          __syncwarp();
         }
+      }
+      if constexpr (MODE == FILL_TMA) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (elect_one()) {
+          tma_store_3d(&tmap, tile, 0, (int)row0, (int)(pos0 * ES / 128));
+          bulk_commit();
+        }
+        ++issued;
+      } else if constexpr (MODE == FILL_STAGED) {
+        __syncwarp();
+        // element stores; CPR lanes cover one 128-byte segment of a row
+        constexpr int CPR = 128 / ES;  // elements per segment
+        constexpr int RPP = 32 / CPR;  // rows per pass (1 for u32, 2 for u64)
+#pragma unroll 4
+        for (int r0 = 0; r0 < 32 * kSegs; r0 += RPP) {
+          const int rs = r0 + lane / CPR;  // (seg, row) flattened seg-major
+          const int seg = rs / 32, r = rs % 32;
+          const int e = lane % CPR;
+          const uint64_t srow = row0 + r;
+          bits v;
+          const uint32_t addr = tile + swz(seg, r, (e * ES) >> 4) + (e * ES & 15);
+          if constexpr (ES == 8) {
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+          } else {
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+          }
+          if (srow < p.nstreams) out[srow * p.ld_out + pos0 + seg * CPR + e] = v;
+        }
+        __syncwarp();
         ++issued;
       }
     }
     for (uint64_t t = 0; t < rem; ++t) {
-      const word x = G::next_flat(s);
+      const bits x = Cv::conv(G::next_flat(s));
       if (valid) {
-        const uint64_t pos = nfull * CH + t;
+        const uint64_t pos = ntiles * CH + t;
         if constexpr (MODE == FILL_POS)
-          out[pos * p.ld_out + stream] = O::conv(x);
+          out[pos * p.ld_out + stream] = x;
         else
-          out[stream * p.ld_out + pos] = O::conv(x);
+          out[stream * p.ld_out + pos] = x;
       }
     }
     if (valid && sout) {
@@ -307,15 +407,21 @@ __global__ void __launch_bounds__(kFillWarps * 32) k_fill(FillParams p, const __
     }
   }
   if constexpr (MODE == FILL_TMA) {
-    if (lane == 0) bulk_wait_all<0>();
+    if (elect_one()) bulk_wait_all<0>();
   }
 }
 
 // ---- K4: fused consumer ---------------------------------------------------------
+//
+// Per output: wrapping sum (IADD3 + IADD3.X) and xor (one LOP3 per two
+// outputs).  MANT adds the exact 128-bit sum (one more IADD3.X with carry) and
+// the sum of the low 11 (w=64) / 8 (w=32) bits, from which the exact sum of
+// the converted doubles / floats follows: mant = (sum - low) >> shift.
+// F64 adds a genuine float64 accumulation of the converted values.
 
 constexpr int kFusedThreads = 256;
 
-template <class G, bool F64>
+template <class G, bool MANT, bool F64>
 __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
   using word = typename G::word;
   constexpr int K = G::k;
@@ -339,19 +445,25 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
 #pragma unroll
     for (int j = 0; j < K; ++j) s[j] = sin[j * p.ld + stream];
     for (uint64_t c = 0; c < nfull; ++c) {
-      word o[CH];
-      gen_chunk<G, CH>(s, o);
       uint32_t lw = 0;
       word xx = 0;
 #pragma unroll
       for (int t = 0; t < CH; t += 2) {
-        add128(slo, shi, (uint64_t)o[t]);
-        add128(slo, shi, (uint64_t)o[t + 1]);
-        xx ^= o[t] ^ o[t + 1];
-        lw += ((uint32_t)o[t] & LOWMASK) + ((uint32_t)o[t + 1] & LOWMASK);
+        const word o0 = G::output(s, t % K);
+        G::step(s, t % K);
+        const word o1 = G::output(s, (t + 1) % K);
+        G::step(s, (t + 1) % K);
+        if constexpr (MANT) {
+          add128(slo, shi, (uint64_t)o0);
+          add128(slo, shi, (uint64_t)o1);
+          lw += ((uint32_t)o0 & LOWMASK) + ((uint32_t)o1 & LOWMASK);
+        } else {
+          slo += (uint64_t)o0 + (uint64_t)o1;
+        }
+        xx ^= o0 ^ o1;
         if constexpr (F64) {
-          fs += __ull2double_rn((uint64_t)o[t] >> SH);
-          fs += __ull2double_rn((uint64_t)o[t + 1] >> SH);
+          fs += __ull2double_rn((uint64_t)o0 >> SH);
+          fs += __ull2double_rn((uint64_t)o1 >> SH);
         }
       }
       sx ^= (uint64_t)xx;
@@ -478,7 +590,6 @@ int launch_fill(const FillParams &p0, cudaStream_t st) {
   using bits = typename Out<OK, typename G::word>::bits;
   constexpr int ES = sizeof(bits);
   FillParams p = p0;
-  p.nunits = (p.nstreams + 31) / 32;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof tmap);
   if constexpr (MODE == FILL_TMA) {
@@ -487,6 +598,7 @@ int launch_fill(const FillParams &p0, cudaStream_t st) {
   }
   auto kern = k_fill<G, OK, MODE>;
   const int smem = MODE == FILL_POS ? 0 : kFillSmem;
+  p.nunits = (p.nstreams + 31) / 32;
   const int dev = current_device();
   static int per_sm[64] = {0};
   if (dev < 0 || dev >= 64) return SLP_ERR_CUDA;
@@ -494,7 +606,7 @@ int launch_fill(const FillParams &p0, cudaStream_t st) {
     if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return cuda_fail("cudaFuncSetAttribute");
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kFillWarps * 32, smem) != cudaSuccess || b < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kFillThreads, smem) != cudaSuccess || b < 1)
       return cuda_fail("occupancy");
     per_sm[dev] = b;
   }
@@ -502,7 +614,7 @@ int launch_fill(const FillParams &p0, cudaStream_t st) {
   uint64_t want = (p.nunits + kFillWarps - 1) / kFillWarps;
   uint64_t cap = (uint64_t)sm_count(dev) * per_sm[dev] * fill_grid_mult();
   const unsigned grid = (unsigned)(want < cap ? want : cap);
-  kern<<<grid, kFillWarps * 32, smem, st>>>(p, tmap);
+  kern<<<grid, kFillThreads, smem, st>>>(p, tmap);
   return check_launch("k_fill");
 }
 
@@ -546,11 +658,11 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
   return SLP_ERR_UNSUPPORTED;
 }
 
-template <class G, bool F64>
+template <class G, bool MANT, bool F64>
 int launch_fused_t(const FusedParams &p0, cudaStream_t st, int *grid_out) {
   FusedParams p = p0;
   p.nunits = (p.nstreams + 31) / 32;
-  auto kern = k_fused<G, F64>;
+  auto kern = k_fused<G, MANT, F64>;
   const int dev = current_device();
   static int per_sm[64] = {0};
   if (dev < 0 || dev >= 64) return SLP_ERR_CUDA;
@@ -573,19 +685,22 @@ int launch_fused_t(const FusedParams &p0, cudaStream_t st, int *grid_out) {
 
 template <class G>
 int fused_impl(const FusedParams &p, int flags, cudaStream_t st, int *grid_out) {
-  if (flags & SLP_FUSE_F64) return launch_fused_t<G, true>(p, st, grid_out);
-  return launch_fused_t<G, false>(p, st, grid_out);
+  if (flags & SLP_FUSE_F64) return launch_fused_t<G, true, true>(p, st, grid_out);
+  if (flags & SLP_FUSE_EXACT) return launch_fused_t<G, true, false>(p, st, grid_out);
+  return launch_fused_t<G, false, false>(p, st, grid_out);
 }
 
 template <class G>
 int fused_grid_cap(int dev) {
-  auto kern = k_fused<G, true>;
+  int best = 1;
   int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kFusedThreads, 0) != cudaSuccess) b = 8;
-  auto kern2 = k_fused<G, false>;
-  int b2 = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, kern2, kFusedThreads, 0) != cudaSuccess) b2 = 8;
-  return sm_count(dev) * (b > b2 ? b : b2);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused<G, true, true>, kFusedThreads, 0) == cudaSuccess)
+    best = b > best ? b : best;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused<G, true, false>, kFusedThreads, 0) == cudaSuccess)
+    best = b > best ? b : best;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused<G, false, false>, kFusedThreads, 0) == cudaSuccess)
+    best = b > best ? b : best;
+  return sm_count(dev) * best;
 }
 
 template <class G>

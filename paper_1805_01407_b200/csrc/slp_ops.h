@@ -44,6 +44,13 @@ struct JumpParams {
   uint64_t src_off, dst_off, batch_stride;
 };
 
+// fill tile geometry (kernel K2): each warp emits tiles of 32 substreams x
+// kSegs x 128 bytes, one 3-D TMA store each; 7 warps x 2 buffers x 8 KiB per
+// CTA -> 2 CTAs (14 warps) per SM
+constexpr int kFillWarps = 7;
+constexpr int kSegs = 2;
+constexpr int kFillBufs = 2;
+
 // up to 16 batches (long-jump blocks) x 16 words, passed by value
 constexpr int kMaxBaseBatches = 16;
 struct BaseStates {

@@ -73,40 +73,49 @@ class Checksum:
     """Exact reduction of a set of outputs (see slp_checksum in include/slp_b200.h)."""
 
     w: int
-    sum: int        # wrapping sum mod 2^64
-    sum_exact: int  # exact integer sum
+    sum: int                # wrapping sum mod 2^64
+    sum_exact: int | None   # exact integer sum (exact mode)
     xor: int
-    mant: int       # exact sum of (x >> 11) (w=64) / (x >> 8) (w=32)
+    mant: int | None        # exact sum of (x >> 11) (w=64) / (x >> 8) (w=32) (exact mode)
     count: int
     fsum_f64: float | None  # float64 accumulation in the kernel (summation order differs)
 
     @property
-    def fsum(self) -> float:
+    def fsum(self) -> float | None:
         """mant * 2^-53 (w=64) / 2^-24 (w=32), correctly rounded once."""
         from fractions import Fraction
 
+        if self.mant is None:
+            return None
         return float(Fraction(self.mant, 1 << (53 if self.w == 64 else 24)))
 
     @classmethod
-    def from_raw(cls, raw: _native.Checksum, w: int, with_f64: bool):
-        exact = (int(raw.sum_hi) << 64) | int(raw.sum_lo)
+    def from_raw(cls, raw: _native.Checksum, w: int, exact: bool, with_f64: bool):
         shift = 11 if w == 64 else 8
-        return cls(w, int(raw.sum_lo), exact, int(raw.xor_all), (exact - int(raw.low_sum)) >> shift,
-                   int(raw.count), float(raw.fsum) if with_f64 else None)
+        if exact:
+            tot = (int(raw.sum_hi) << 64) | int(raw.sum_lo)
+            mant = (tot - int(raw.low_sum)) >> shift
+        else:
+            tot = mant = None
+        return cls(w, int(raw.sum_lo), tot, int(raw.xor_all), mant, int(raw.count),
+                   float(raw.fsum) if with_f64 else None)
 
     @classmethod
     def fold(cls, parts):
         """Combine checksums of disjoint output sets (order-independent, exact)."""
         parts = list(parts)
         w = parts[0].w
-        exact = sum(p.sum_exact for p in parts)
         x = 0
         for p in parts:
             x ^= p.xor
+        exact = mant = None
+        if all(p.sum_exact is not None for p in parts):
+            exact = sum(p.sum_exact for p in parts)
+            mant = sum(p.mant for p in parts)
         f64 = None
         if all(p.fsum_f64 is not None for p in parts):
             f64 = float(sum(p.fsum_f64 for p in parts))
-        return cls(w, exact & ((1 << 64) - 1), exact, x, sum(p.mant for p in parts),
+        return cls(w, sum(p.sum for p in parts) & ((1 << 64) - 1), exact, x, mant,
                    sum(p.count for p in parts), f64)
 
 
@@ -121,11 +130,11 @@ def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor
     k = spec.kind.k
     if states.dim() != 2 or states.shape[0] != k or states.dtype != _word_dtype(spec.kind.w) or not states.is_cuda:
         raise ValueError(f"states must be a CUDA ({k}, ld) {_word_dtype(spec.kind.w)} tensor")
-    if not states.is_contiguous():
-        raise ValueError("states must be contiguous")
-    ld = states.shape[1]
-    n = ld if nstreams is None else int(nstreams)
-    if T < 0 or n < 0 or n > ld:
+    if states.stride(1) != 1 or (k > 1 and states.stride(0) < states.shape[1]):
+        raise ValueError("states must have unit column stride (a column slice of a (k, ld) tensor)")
+    ld = states.stride(0) if k > 1 else states.shape[1]
+    n = states.shape[1] if nstreams is None else int(nstreams)
+    if T < 0 or n < 0 or n > states.shape[1]:
         raise ValueError("bad T / nstreams")
     dt = _out_dtype(spec, kind)
     if layout not in _LAYOUT:
@@ -140,8 +149,9 @@ def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor
     if states_out is None:
         sout = states.data_ptr() if advance else None
     else:
-        if states_out.shape != states.shape or states_out.dtype != states.dtype:
-            raise ValueError("states_out must match states")
+        if states_out.shape != states.shape or states_out.dtype != states.dtype \
+                or states_out.stride() != states.stride():
+            raise ValueError("states_out must match states (shape, dtype, strides)")
         sout = states_out.data_ptr()
     L = _native.lib()
     with torch.cuda.device(states.device):
@@ -166,8 +176,8 @@ def _workspace(gid: int, dev: torch.device) -> torch.Tensor:
     return ws
 
 
-def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, f64: bool = False,
-                         nstreams: int | None = None, advance: bool = True,
+def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, exact: bool = True,
+                         f64: bool = False, nstreams: int | None = None, advance: bool = True,
                          result: torch.Tensor | None = None) -> torch.Tensor:
     """Kernel K4: reduce T outputs of each substream in-kernel; returns the
     48-byte slp_checksum as a uint8 CUDA tensor (no host synchronisation)."""
@@ -180,7 +190,7 @@ def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, f
     ws = _workspace(gid, dev)
     if result is None:
         result = torch.empty(_native.CHECKSUM_BYTES, dtype=torch.uint8, device=dev)
-    flags = _native.FUSE_INT | (_native.FUSE_F64 if f64 else 0)
+    flags = _native.FUSE_INT | (_native.FUSE_EXACT if exact else 0) | (_native.FUSE_F64 if f64 else 0)
     L = _native.lib()
     with torch.cuda.device(dev):
         rc = L.slp_fused(gid, ctypes.c_void_p(states.data_ptr()),
@@ -191,15 +201,51 @@ def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, f
     return result
 
 
-def decode_checksum(raw: torch.Tensor | bytes, w: int, f64: bool) -> Checksum:
+def decode_checksum(raw: torch.Tensor | bytes, w: int, exact: bool = True, f64: bool = False) -> Checksum:
     b = bytes(raw.cpu().numpy().tobytes()) if isinstance(raw, torch.Tensor) else bytes(raw)
-    return Checksum.from_raw(_native.Checksum.from_buffer_copy(b), w, f64)
+    return Checksum.from_raw(_native.Checksum.from_buffer_copy(b), w, exact or f64, f64)
 
 
-def fused_checksum(spec: GeneratorSpec, states: torch.Tensor, T: int, *, f64: bool = False,
+def fused_checksum(spec: GeneratorSpec, states: torch.Tensor, T: int, *, exact: bool = True, f64: bool = False,
                    nstreams: int | None = None, advance: bool = True) -> Checksum:
-    raw = fused_checksum_async(spec, states, T, f64=f64, nstreams=nstreams, advance=advance)
-    return decode_checksum(raw, spec.kind.w, f64)
+    raw = fused_checksum_async(spec, states, T, exact=exact, f64=f64, nstreams=nstreams, advance=advance)
+    return decode_checksum(raw, spec.kind.w, exact, f64)
+
+
+def fill_to_host(spec: GeneratorSpec, states: torch.Tensor, T: int, host_out: torch.Tensor, *,
+                 kind: str = "native", slice_streams: int = 1 << 17, _bufs: list | None = None) -> torch.Tensor:
+    """Stream-major fill delivered to HOST memory: the GPU generates slices of
+    ``slice_streams`` substreams into two device buffers while a copy stream
+    moves the previous slice to ``host_out`` (pinned (n, T) tensor), so the
+    device-to-host copy overlaps generation.  States advance in place."""
+    n = states.shape[1]
+    dev = states.device
+    if tuple(host_out.shape) != (n, T) or host_out.device.type != "cpu":
+        raise ValueError(f"host_out must be a ({n}, {T}) CPU tensor")
+    dt = _out_dtype(spec, kind)
+    if host_out.dtype != dt:
+        raise ValueError(f"host_out dtype must be {dt}")
+    sl = max(1, min(slice_streams, n))
+    bufs = _bufs if _bufs is not None else [torch.empty((sl, T), dtype=dt, device=dev) for _ in range(2)]
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    done = [None, None]
+    for i, a in enumerate(range(0, n, sl)):
+        b = min(n, a + sl)
+        buf = bufs[i & 1][: b - a]
+        if done[i & 1] is not None:
+            compute.wait_event(done[i & 1])
+        fill(spec, states[:, a:b], T, out=buf, kind=kind)
+        ready = torch.cuda.Event()
+        ready.record(compute)
+        with torch.cuda.stream(copy):
+            copy.wait_event(ready)
+            host_out[a:b].copy_(buf, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        done[i & 1] = ev
+    compute.wait_stream(copy)
+    return host_out
 
 
 class Substreams:
@@ -271,11 +317,13 @@ class Substreams:
     def fill(self, T: int, *, out=None, kind: str = "native", layout: str = "stream", advance: bool = True):
         return fill(self.spec, self.states, T, out=out, kind=kind, layout=layout, advance=advance)
 
-    def checksum(self, T: int, *, f64: bool = False, advance: bool = True) -> Checksum:
-        return fused_checksum(self.spec, self.states, T, f64=f64, advance=advance)
+    def checksum(self, T: int, *, exact: bool = True, f64: bool = False, advance: bool = True) -> Checksum:
+        return fused_checksum(self.spec, self.states, T, exact=exact, f64=f64, advance=advance)
 
-    def checksum_async(self, T: int, *, f64: bool = False, advance: bool = True, result=None) -> torch.Tensor:
-        return fused_checksum_async(self.spec, self.states, T, f64=f64, advance=advance, result=result)
+    def checksum_async(self, T: int, *, exact: bool = True, f64: bool = False, advance: bool = True,
+                       result=None) -> torch.Tensor:
+        return fused_checksum_async(self.spec, self.states, T, exact=exact, f64=f64, advance=advance,
+                                    result=result)
 
     def jump(self, jp: JumpPolynomial) -> "Substreams":
         """Advance every substream by jp.step_count steps (kernel K1, in place)."""
