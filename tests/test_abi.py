@@ -1,0 +1,49 @@
+"""The C-ABI library loads and exports every entry point include/slp_b200.h
+declares (no device calls: runs without a GPU)."""
+
+import ctypes
+import os
+import re
+
+from paper_1805_01407_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    with open(os.path.join(ROOT, "include", "slp_b200.h")) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(slp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_expected_surface():
+    names = declared_functions()
+    for must in ("slp_fill", "slp_fused", "slp_init_substreams", "slp_jump_states", "slp_char_poly",
+                 "slp_jump_poly", "slp_host_jump", "slp_generator_id"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_covers_header():
+    assert set(declared_functions()) == set(_native.SIGNATURES)
+    L = _native.lib()
+    assert b"sm_100a" in L.slp_build_info()
+    assert L.slp_status_str(_native.SLP_ERR_ZERO_STATE)
+
+
+def test_device_entry_points_reject_bad_arguments_without_touching_the_gpu():
+    L = _native.lib()
+    # unknown generator / null pointers are rejected before any CUDA call
+    assert L.slp_fill(999, None, None, 0, 0, 0, 0, 0, None, 0, None) == _native.SLP_ERR_UNKNOWN_GENERATOR
+    assert L.slp_fill(8, None, None, 0, 0, 0, 0, 0, None, 0, None) == _native.SLP_ERR_INVALID
+    assert L.slp_fused(8, None, None, 0, 0, 0, 1, None, None, 0, None) == _native.SLP_ERR_INVALID
+    assert L.slp_init_substreams(8, None, 1, None, 0, None, 1, 1, None) == _native.SLP_ERR_INVALID
+    zero = (ctypes.c_uint64 * 4)()
+    assert L.slp_jump_states(8, zero, 4, ctypes.c_void_p(16), 4, ctypes.c_void_p(16), 4, 4, None) \
+        == _native.SLP_ERR_ZERO_STATE
