@@ -3,9 +3,9 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 CSRC := paper_1805_01407_b200/csrc
 LIBDIR := paper_1805_01407_b200/_lib
-OBJDIR := build/obj
+OBJDIR := build/obj$(if $(VARIANT),_$(VARIANT),)
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall -Xptxas -v -I include
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall -Xptxas -v -I include $(EXTRA)
 CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -I include
 
 INST := $(wildcard $(CSRC)/slp_inst_*.cu)
@@ -13,6 +13,13 @@ OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(INST)) $(OBJDIR)/slp_api.o $(OBJ
 HDRS := $(wildcard $(CSRC)/*.h $(CSRC)/*.cuh) include/slp_b200.h
 
 all: $(LIBDIR)/libslp_b200.so oracle
+
+# A/B experiment builds: make variant VARIANT=name EXTRA="-DSLP_ROT_POLICY=0"
+variant: variants/libslp_$(VARIANT).so
+
+variants/libslp_$(VARIANT).so: $(OBJS)
+	@mkdir -p variants
+	$(NVCC) -shared $(ARCH) -cudart static -o $@ $(OBJS)
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -33,4 +40,4 @@ clean:
 	rm -rf build $(LIBDIR)/*.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all clean oracle
+.PHONY: all clean oracle variant

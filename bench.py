@@ -237,7 +237,10 @@ def run_ours(args):
                 "alg_bytes_per_launch": alg_bytes,
                 "alg_bytes_per_unit": "8 B per u64 output + 64 B state read/write per substream per launch",
                 "kernel": "k_fill<xoshiro256**, u64, TMA>", "launch_ms": round(launch_ms, 4),
-                "frac_of_8TBps_spec": round(achieved / 8000.0, 4)}
+                "frac_of_8TBps_spec": round(achieved / 8000.0, 4),
+                "frac_of_write_pattern_ceiling": round(achieved / 5836.0, 4),
+                "write_pattern_ceiling_note": "5836 GB/s = TMA-only store of the same stream-major pattern "
+                                              "(256 B row pieces, no generation), profiles/round1_write_patterns.md"}
 
     # e2e: public API from the seed to HOST memory, every step: substream init
     # (H2D: the base state, k words) + fill + D2H of all outputs (pinned), overlapped
@@ -266,6 +269,32 @@ def run_ours(args):
                "ms_per_step": round(e_ms / args.e2e_steps, 3), "wall_s": round(wall, 3)}
         del host, bufs
 
+    # the same API call when the consumer is on the GPU: per step the base state
+    # goes in (kernel parameters), substreams are initialised (K1) and filled
+    # (K2) into a device tensor, and one output word is read back as the result
+    e2e_dev = None
+    if args.e2e_steps > 0:
+        outd = torch.empty((N_STREAMS, T), dtype=torch.uint64, device=dev)
+        res_host = torch.empty(1, dtype=torch.uint64, pin_memory=True)
+        for i in range(args.e2e_steps + 3):
+            if i == 3:
+                barrier()
+                torch.cuda.synchronize()
+                f0 = torch.cuda.Event(enable_timing=True)
+                f0.record()
+            s3 = D.Substreams.from_seed(spec, SEED, N_STREAMS, first_block=rank)
+            s3.fill(T, out=outd)
+            res_host.copy_(outd[-1, -1:], non_blocking=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f1.record()
+        torch.cuda.synchronize()
+        f_ms = max_over_ranks(f0.elapsed_time(f1))
+        e2e_dev = {"value": outputs_per_step * args.e2e_steps / (f_ms / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": k * 8, "d2h_bytes_per_step": 8,
+                   "api": "Substreams.from_seed + Substreams.fill (device tensor), init included",
+                   "ms_per_step": round(f_ms / args.e2e_steps, 4)}
+        del outd
+
     extra = {}
     if args.extra:
         extra = run_extra(spec, dev, rank)
@@ -278,6 +307,7 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, SplitMix64)",
                 "config": config(world), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+                "e2e_device_resident": e2e_dev,
                 "clocks": clocks.summary(), "gpu_launches": args.steps,
                 "init_ms_2^20_substreams": round(init_ms, 3)}
         line.update(extra)
@@ -295,25 +325,20 @@ def run_extra(spec, dev, rank):
     res = {}
     sub = D.Substreams.from_seed(spec, SEED, N_STREAMS, first_block=rank)
     raw = torch.empty(48, dtype=torch.uint8, device=dev)
-    for _ in range(3):
-        sub.checksum_async(T, result=raw)
-    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 50
-    e0.record()
-    for _ in range(reps):
-        sub.checksum_async(T, result=raw)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    res["fused_int"] = {"outputs_per_s": N_STREAMS * T / (ms / 1e3), "ms_per_step": ms}
-    e0.record()
-    for _ in range(reps):
-        sub.checksum_async(T, f64=True, result=raw)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    res["fused_int_f64"] = {"outputs_per_s": N_STREAMS * T / (ms / 1e3), "ms_per_step": ms}
+    for label, kw in (("fused_int", dict(exact=False)), ("fused_exact", dict(exact=True)),
+                      ("fused_exact_f64", dict(exact=True, f64=True))):
+        for _ in range(3):
+            sub.checksum_async(T, result=raw, **kw)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            sub.checksum_async(T, result=raw, **kw)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        res[label] = {"outputs_per_s": N_STREAMS * T / (ms / 1e3), "ms_per_step": ms}
     out = torch.empty((N_STREAMS, T), dtype=torch.float64, device=dev)
     sub.fill(T, out=out, kind="f64")
     e0.record()

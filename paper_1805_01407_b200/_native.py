@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libslp_b200.so")
+LIB_PATH = os.environ.get("SLP_LIB") or os.path.join(_HERE, "_lib", "libslp_b200.so")  # SLP_LIB: A/B builds
 
 # status codes (include/slp_b200.h)
 SLP_OK = 0

@@ -374,6 +374,7 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
   p.T = T;
   p.partials = workspace;
   p.workspace_bytes = workspace_bytes;
+  p.one = 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int grid = 0;
   int rc = ops->fused(p, flags, st, &grid);

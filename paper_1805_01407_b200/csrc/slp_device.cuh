@@ -35,11 +35,33 @@ struct WordOf<32> {
   using type = uint32_t;
 };
 
-// Word operations.  64-bit words are manipulated as explicit 32-bit halves:
-// rotations are two funnel shifts (SHF.L.W), constant shifts one funnel shift
-// plus one plain shift, and multiplication by a constant C < 2^32 is one
-// IMAD.WIDE.U32 plus one IMAD (three for a 64-bit constant), which is what
-// the SASS count per output is built on.
+// PTX wide multiply-adds: ptxas keeps these on the FMA pipe (IMAD.WIDE.U32 /
+// IMAD), even for power-of-two multipliers, which is how shifts and rotations
+// are moved off the ALU pipe below.
+__device__ __forceinline__ uint64_t mulw(uint32_t a, uint32_t b) {
+  uint64_t d;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t madw(uint32_t a, uint32_t b, uint64_t c) {
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// Word operations.  64-bit words are manipulated as explicit 32-bit halves.
+// The generators are integer-issue bound on the ALU pipe (LOP3/SHF/IADD3,
+// profiles/), so every rotation has two forms:
+//   rotl   : two funnel shifts (SHF.L.W)                 -> 2 ALU
+//   rotl_f : three wide multiply-adds by 2^r             -> 3 FMA
+// and the kernels pick, per generator, the mix that balances the two pipes
+// (Gen::best_mask).  Constant left shifts are 2 FMA (IMAD.WIDE + IMAD),
+// multiplication by a constant < 2^32 is 2 FMA (3 for a 64-bit constant).
 template <int W>
 struct WOps;
 
@@ -49,6 +71,10 @@ struct WOps<32> {
   template <int R>
   static __device__ __forceinline__ word rotl(word x) {
     return __funnelshift_l(x, x, R);
+  }
+  template <int R>
+  static __device__ __forceinline__ word rotl_f(word x) {
+    return __funnelshift_l(x, x, R);  // no cheaper FMA form for one 32-bit word
   }
   template <int B>
   static __device__ __forceinline__ word shl(word x) {
@@ -82,10 +108,27 @@ struct WOps<64> {
     if constexpr (r == 0) return pack(l, h);
     return pack(__funnelshift_l(h, l, r), __funnelshift_l(l, h, r));
   }
+  template <int R>
+  static __device__ __forceinline__ word rotl_f(word x) {
+    uint32_t l = lo(x), h = hi(x);
+    if constexpr (R >= 32) {
+      const uint32_t t = l;
+      l = h;
+      h = t;
+    }
+    constexpr int r = R & 31;
+    if constexpr (r == 0) return pack(l, h);
+    constexpr uint32_t m = 1u << r;
+    const uint64_t w1 = mulw(l, m);                          // (l << r, l >> (32 - r))
+    const uint64_t w2 = madw(h, m, w1 >> 32);                // low: (h << r) | (l >> (32 - r))
+    const uint64_t w3 = madw(l, m, w2 >> 32);                // low: (l << r) | (h >> (32 - r))
+    return pack((uint32_t)w3, (uint32_t)w2);
+  }
   template <int B>
   static __device__ __forceinline__ word shl(word x) {
     if constexpr (B >= 32) return pack(0u, lo(x) << (B - 32));
-    return pack(lo(x) << B, __funnelshift_l(lo(x), hi(x), B));
+    const uint64_t w = mulw(lo(x), 1u << B);
+    return pack((uint32_t)w, madlo(hi(x), 1u << B, (uint32_t)(w >> 32)));
   }
   template <int B>
   static __device__ __forceinline__ word shr(word x) {
@@ -94,11 +137,25 @@ struct WOps<64> {
   }
   template <unsigned long long C>
   static __device__ __forceinline__ word mulc(word x) {
-    const uint64_t p = (uint64_t)lo(x) * (uint32_t)C;  // IMAD.WIDE.U32
-    uint32_t h = hi(x) * (uint32_t)C + (uint32_t)(p >> 32);
-    if constexpr ((C >> 32) != 0) h += lo(x) * (uint32_t)(C >> 32);
+    const uint64_t p = mulw(lo(x), (uint32_t)C);
+    uint32_t h = madlo(hi(x), (uint32_t)C, (uint32_t)(p >> 32));
+    if constexpr ((C >> 32) != 0) h = madlo(lo(x), (uint32_t)(C >> 32), h);
     return pack((uint32_t)p, h);
   }
+};
+
+// Build-time policy switches (A/B experiments, profiles/): rotation pipe
+// balancing and the fused accumulator form.
+#ifndef SLP_ROT_POLICY
+#define SLP_ROT_POLICY 0  // 0: all rotations on the ALU; 1: Gen::best_mask (A/B: no gain, ptxas re-normalises)
+#endif
+#ifndef SLP_SUM_POLICY
+#define SLP_SUM_POLICY 0  // 0: IADD3 carry chains; 1: IMAD.WIDE accumulators
+#endif
+
+// Pipe cost of one output, in warp instructions per 32 outputs
+struct PipeCost {
+  int alu, fma;
 };
 
 template <int FAM, int K, int W, int A, int B, int C, int SC, int WI, int WJ, unsigned long long S_, int R_,
@@ -112,11 +169,74 @@ struct Gen {
   static constexpr int pw = n / 64;  // u64 words per jump polynomial (degree < n)
   static constexpr bool ring = FAM != SLP_FAM_XOSHIRO;
 
+  // Rotation sites that may run on either pipe (bit set in a mask = FMA form):
+  //   bit 0: engine rotation by A (xoroshiro) / by B (xoshiro)
+  //   bit 1: engine rotation by C (xoroshiro)
+  //   bit 2: scrambler rotation by R (++ and **)
+  static constexpr int kSites = (W == 64 ? ((FAM == SLP_FAM_XOROSHIRO ? 3 : (FAM == SLP_FAM_XOSHIRO ? 1 : 0)) |
+                                            ((SC == SLP_SC_PLUSPLUS || SC == SLP_SC_STARSTAR) ? 4 : 0))
+                                         : 0);
+
+  // ALU/FMA instructions per output outside the rotation sites (SASS counts, profiles/)
+  static __host__ __device__ constexpr PipeCost fixed() {
+    PipeCost c{0, 0};
+    const int h = W == 64 ? 2 : 1;  // 32-bit halves per word
+    if (FAM == SLP_FAM_XOROSHIRO) {
+      c.alu += 2 * h;               // xl = s[l] ^ s0; new = rot ^ xl ^ shl (3-input LOP3)
+      c.fma += W == 64 ? 2 : 1;     // xl << B
+    } else if (FAM == SLP_FAM_XORSHIFT) {
+      c.alu += 5 * h;
+      c.fma += 2;
+    } else {
+      c.alu += (K == 4 ? 4 : 7) * h;  // the xor network (LOP3 fuses pairs)
+      c.fma += W == 64 ? 2 : 1;       // t = s1 << A
+    }
+    if (W == 32) c.alu += FAM == SLP_FAM_XOROSHIRO ? 2 : 1;  // 32-bit rotations always on the ALU
+    if (SC == SLP_SC_PLUS) c.alu += h;
+    if (SC == SLP_SC_STAR) c.fma += W == 64 ? ((S_ >> 32) ? 3 : 2) : 1;
+    if (SC == SLP_SC_PLUSPLUS) c.alu += 2 * h + (W == 32 ? 1 : 0);
+    if (SC == SLP_SC_STARSTAR) c.fma += W == 64 ? 4 : 2, c.alu += W == 32 ? 1 : 0;
+    return c;
+  }
+  // best rotation mask given extra per-output work of the calling kernel
+  static __host__ __device__ constexpr int best_mask(int extra_alu, int extra_fma) {
+    if (SLP_ROT_POLICY == 0) return 0;
+    const PipeCost f = fixed();
+    int best = 0, best_cost = 1 << 30;
+    for (int m = 0; m < 8; ++m) {
+      if ((m & ~kSites) != 0) continue;
+      int alu = f.alu + extra_alu, fma = f.fma + extra_fma;
+      for (int bit = 0; bit < 3; ++bit) {
+        if (!(kSites & (1 << bit))) continue;
+        if (m & (1 << bit))
+          fma += 3;
+        else
+          alu += 2;
+      }
+      const int cost = (2 * alu > 2 * fma ? 2 * alu : 2 * fma) > alu + fma ? (2 * alu > 2 * fma ? 2 * alu : 2 * fma)
+                                                                            : alu + fma;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = m;
+      }
+    }
+    return best;
+  }
+
+  template <int M, int RR>
+  static __device__ __forceinline__ word rot(word x) {
+    if constexpr (M != 0)
+      return O::template rotl_f<RR>(x);
+    else
+      return O::template rotl<RR>(x);
+  }
+
   // register slot of flat word j when the ring offset is o (constant after unrolling)
   static __device__ __forceinline__ constexpr int slot(int o, int j) { return ring ? (o + j) % K : j; }
 
   // scramblers.py:84-95, applied to the current (pre-step) state
-  static __device__ __forceinline__ word output(const word (&s)[K], int o) {
+  template <int M>
+  static __device__ __forceinline__ word output_m(const word (&s)[K], int o) {
     const word xi = s[slot(o, WI)];
     if constexpr (SC == SLP_SC_NONE) {
       return xi;
@@ -125,21 +245,22 @@ struct Gen {
     } else if constexpr (SC == SLP_SC_STAR) {
       return O::template mulc<S_>(xi);
     } else if constexpr (SC == SLP_SC_PLUSPLUS) {
-      return (word)(O::template rotl<R_>((word)(xi + s[slot(o, WJ)])) + xi);
+      return (word)(rot<M & 4, R_>((word)(xi + s[slot(o, WJ)])) + xi);
     } else {
-      return O::template mulc<T_>(O::template rotl<R_>(O::template mulc<S_>(xi)));
+      return O::template mulc<T_>(rot<M & 4, R_>(O::template mulc<S_>(xi)));
     }
   }
 
   // one engine step in the flat view (engines.py:100-140).  For ring engines
   // the flat view moves by one slot: the caller's next offset is o + 1.
-  static __device__ __forceinline__ void step(word (&s)[K], int o) {
+  template <int M>
+  static __device__ __forceinline__ void step_m(word (&s)[K], int o) {
     if constexpr (FAM == SLP_FAM_XOROSHIRO) {
       const int i0 = slot(o, 0), il = slot(o, K - 1);
       const word x0 = s[i0];
       const word xl = s[il] ^ x0;
-      s[il] = O::template rotl<A>(x0) ^ xl ^ O::template shl<B>(xl);
-      s[i0] = O::template rotl<C>(xl);
+      s[il] = rot<M & 1, A>(x0) ^ xl ^ O::template shl<B>(xl);
+      s[i0] = rot<M & 2, C>(xl);
     } else if constexpr (FAM == SLP_FAM_XORSHIFT) {
       const int i0 = slot(o, 0), i1 = slot(o, 1);
       const word s0 = s[i0], s1 = s[i1];
@@ -152,7 +273,7 @@ struct Gen {
       s[1] ^= s[2];
       s[0] ^= s[3];
       s[2] ^= t;
-      s[3] = O::template rotl<B>(s[3]);
+      s[3] = rot<M & 1, B>(s[3]);
     } else {
       const word t = O::template shl<A>(s[1]);
       s[2] ^= s[0];
@@ -164,9 +285,13 @@ struct Gen {
       s[0] ^= s[6];
       s[6] ^= s[7];
       s[6] ^= t;
-      s[7] = O::template rotl<B>(s[7]);
+      s[7] = rot<M & 1, B>(s[7]);
     }
   }
+
+  // defaults (all-ALU rotations): jump kernel and tails
+  static __device__ __forceinline__ word output(const word (&s)[K], int o) { return output_m<0>(s, o); }
+  static __device__ __forceinline__ void step(word (&s)[K], int o) { step_m<0>(s, o); }
 
   // one output + step, registers left in flat order (tails of odd length)
   static __device__ __forceinline__ word next_flat(word (&s)[K]) {
@@ -299,6 +424,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
   constexpr int CH = kTileRowBytes / ES;                          // outputs per substream per tile
   constexpr int EPC = 16 / ES;                                    // elements per 16-byte chunk
   static_assert(!G::ring || CH % K == 0, "tile must cover whole ring periods");
+  constexpr int MSK = G::best_mask(0, 0);  // rotation pipe mix (ALU vs FMA), see Gen::best_mask
   const int lane = threadIdx.x & 31;
   const int warp = warp_uniform();  // keeps TMA coordinates in uniform registers
 
@@ -338,8 +464,8 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
 #pragma unroll
         for (int i = 0; i < EPC; ++i) {
           const int o = (e + i) % K;
-          v[i] = Cv::conv(G::output(s, o));
-          G::step(s, o);
+          v[i] = Cv::conv(G::template output_m<MSK>(s, o));
+          G::template step_m<MSK>(s, o);
         }
         if constexpr (MODE == FILL_POS) {
           if (valid) {
@@ -436,6 +562,14 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
   const uint64_t nfull = p.T / CH;
   const uint64_t rem = p.T - nfull * CH;
 
+  // Per-output accumulation runs mostly on the FMA pipe (the generator
+  // itself saturates the ALU pipe): sum of the low and of the high 32-bit
+  // halves in two 64-bit IMAD.WIDE accumulators (x_half * one + acc, `one`
+  // is an opaque 1 from the parameters so ptxas cannot turn it into IADD3);
+  // together they give the EXACT sum.  xor: one 3-input LOP3 per output pair
+  // and half.  MANT: low-bit sum = LOP3 + IMAD.
+  constexpr int MSK = G::best_mask(G::w == 64 ? 1 : 1, (G::w == 64 ? 2 : 1) + (MANT ? 1 : 0));
+  const uint32_t one = p.one;
   uint64_t slo = 0, shi = 0, sx = 0, slow = 0;
   double fs = 0.0;
   for (uint64_t u = (uint64_t)blockIdx.x * WPB + warp; u < p.nunits; u += (uint64_t)gridDim.x * WPB) {
@@ -444,15 +578,28 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
     word s[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) s[j] = sin[j * p.ld + stream];
+    uint64_t acc_lo = 0, acc_hi = 0;  // sums of 32-bit halves (< 2^32 terms per substream)
     for (uint64_t c = 0; c < nfull; ++c) {
       uint32_t lw = 0;
       word xx = 0;
 #pragma unroll
       for (int t = 0; t < CH; t += 2) {
-        const word o0 = G::output(s, t % K);
-        G::step(s, t % K);
-        const word o1 = G::output(s, (t + 1) % K);
-        G::step(s, (t + 1) % K);
+        const word o0 = G::template output_m<MSK>(s, t % K);
+        G::template step_m<MSK>(s, t % K);
+        const word o1 = G::template output_m<MSK>(s, (t + 1) % K);
+        G::template step_m<MSK>(s, (t + 1) % K);
+#if SLP_SUM_POLICY == 1
+        acc_lo = madw((uint32_t)o0, one, acc_lo);
+        acc_lo = madw((uint32_t)o1, one, acc_lo);
+        if constexpr (G::w == 64) {
+          acc_hi = madw((uint32_t)((uint64_t)o0 >> 32), one, acc_hi);
+          acc_hi = madw((uint32_t)((uint64_t)o1 >> 32), one, acc_hi);
+        }
+        if constexpr (MANT) {
+          lw = madlo((uint32_t)o0 & LOWMASK, one, lw);
+          lw = madlo((uint32_t)o1 & LOWMASK, one, lw);
+        }
+#else
         if constexpr (MANT) {
           add128(slo, shi, (uint64_t)o0);
           add128(slo, shi, (uint64_t)o1);
@@ -460,6 +607,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
         } else {
           slo += (uint64_t)o0 + (uint64_t)o1;
         }
+#endif
         xx ^= o0 ^ o1;
         if constexpr (F64) {
           fs += __ull2double_rn((uint64_t)o0 >> SH);
@@ -471,11 +619,16 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
     }
     for (uint64_t t = 0; t < rem; ++t) {
       const word x = G::next_flat(s);
-      add128(slo, shi, (uint64_t)x);
+      acc_lo += (uint32_t)x;
+      if constexpr (G::w == 64) acc_hi += (uint32_t)((uint64_t)x >> 32);
       sx ^= (uint64_t)x;
       slow += (uint32_t)x & LOWMASK;
       if constexpr (F64) fs += __ull2double_rn((uint64_t)x >> SH);
     }
+    // fold this substream's exact sum acc_lo + acc_hi * 2^32 into the 128-bit total
+    add128(slo, shi, acc_lo);
+    add128(slo, shi, acc_hi << 32);
+    shi += acc_hi >> 32;
     if (sout) {
 #pragma unroll
       for (int j = 0; j < K; ++j) sout[j * p.ld + stream] = s[j];

@@ -28,6 +28,7 @@ struct FusedParams {
   void *partials;          // slp_checksum[grid]
   size_t workspace_bytes;  // bytes available at partials
   uint64_t nunits;
+  uint32_t one;            // = 1, opaque to ptxas (keeps accumulations on IMAD)
 };
 
 struct JumpParams {
