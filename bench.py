@@ -320,6 +320,7 @@ def run_extra(spec, dev, rank):
     """Fused mode (K4) on the same substreams + init cost, for DESIGN.md."""
     import torch
 
+    import paper_1805_01407_b200 as P
     from paper_1805_01407_b200 import device as D
 
     res = {}
@@ -339,6 +340,33 @@ def run_extra(spec, dev, rank):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         res[label] = {"outputs_per_s": N_STREAMS * T / (ms / 1e3), "ms_per_step": ms}
+    # config 5 whole job: 2^34 outputs = 8 long-jump blocks x 2^18 substreams x 2^13,
+    # blocks b == rank (mod world), fused exact checksum per GPU, one all_gather
+    import torch.distributed as dist
+
+    from paper_1805_01407_b200.multigpu import sharded_checksum
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    golden = {}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "checksums_big.json")) as f:
+            golden = json.load(f)
+    except OSError:
+        pass
+    c5 = {}
+    for name in ("xoshiro512starstar", "xoroshiro1024plusplus"):
+        s5 = P.get_spec(name)
+        sharded_checksum(s5, 42, 8, 1 << 10, 1 << 6, rank=rank, world=world, device=dev)  # warm plans
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        total, _ = sharded_checksum(s5, 42, 8, 1 << 18, 1 << 13, rank=rank, world=world, device=dev)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        g = golden.get(f"c5/{name}", {})
+        c5[name] = {"job_s": round(dt, 4), "outputs_per_s": (1 << 34) / dt,
+                    "matches_reference": bool(g) and hex(total.sum) == g["sum"] and hex(total.xor) == g["xor"]
+                    and hex(total.mant) == g["mant"], "sum": hex(total.sum), "xor": hex(total.xor)}
+    res["config5_job"] = c5
     out = torch.empty((N_STREAMS, T), dtype=torch.float64, device=dev)
     sub.fill(T, out=out, kind="f64")
     e0.record()

@@ -9,6 +9,8 @@
 //   x^e mod P             gf2.py:214-227 (square-and-multiply)
 //   jump by polynomial    generators.py:315-334
 //   lane doubling         generators.py:450-459 (here: radix-8 rounds, see init_plan)
+#include <immintrin.h>
+
 #include <cstring>
 #include <map>
 #include <memory>
@@ -109,8 +111,16 @@ void poly_trim(Poly &p) {
   while (!p.empty() && p.back() == 0) p.pop_back();
 }
 
-// 64 x 64 -> 128 carry-less product (portable 4-bit window)
-static inline void clmul64(uint64_t a, uint64_t b, uint64_t &lo, uint64_t &hi) {
+// 64 x 64 -> 128 carry-less product: PCLMULQDQ when the host CPU has it,
+// else a portable 4-bit window.
+__attribute__((target("pclmul,sse4.1"))) static void clmul64_hw(uint64_t a, uint64_t b, uint64_t &lo,
+                                                                  uint64_t &hi) {
+  const __m128i r = _mm_clmulepi64_si128(_mm_cvtsi64_si128((long long)a), _mm_cvtsi64_si128((long long)b), 0);
+  lo = (uint64_t)_mm_cvtsi128_si64(r);
+  hi = (uint64_t)_mm_extract_epi64(r, 1);
+}
+
+static void clmul64_sw(uint64_t a, uint64_t b, uint64_t &lo, uint64_t &hi) {
   uint64_t tbl_lo[16], tbl_hi[16];
   tbl_lo[0] = 0;
   tbl_hi[0] = 0;
@@ -125,13 +135,21 @@ static inline void clmul64(uint64_t a, uint64_t b, uint64_t &lo, uint64_t &hi) {
   lo = 0;
   hi = 0;
   for (int i = 60; i >= 0; i -= 4) {
-    // shift accumulator left by 4 then add table[nibble]
     hi = (hi << 4) | (lo >> 60);
     lo <<= 4;
     unsigned nib = (a >> i) & 15;
     lo ^= tbl_lo[nib];
     hi ^= tbl_hi[nib];
   }
+}
+
+static const bool g_has_pclmul = __builtin_cpu_supports("pclmul") && __builtin_cpu_supports("sse4.1");
+
+static inline void clmul64(uint64_t a, uint64_t b, uint64_t &lo, uint64_t &hi) {
+  if (g_has_pclmul)
+    clmul64_hw(a, b, lo, hi);
+  else
+    clmul64_sw(a, b, lo, hi);
 }
 
 Poly poly_mul(const Poly &a, const Poly &b) {
@@ -151,6 +169,7 @@ Poly poly_mul(const Poly &a, const Poly &b) {
   return r;
 }
 
+// generic long division remainder (bit-serial); used once per modulus
 Poly poly_mod(Poly a, const Poly &m) {
   const int dm = poly_degree(m);
   if (dm < 0) throw std::invalid_argument("polynomial modulus is zero");
@@ -164,7 +183,6 @@ Poly poly_mod(Poly a, const Poly &m) {
       a[j + ws] ^= v << bs;
       if (bs && j + ws + 1 < a.size()) a[j + ws + 1] ^= v >> (64 - bs);
     }
-    // find the new top bit, scanning down from da
     int wi = da / 64;
     while (wi >= 0 && a[wi] == 0) --wi;
     da = wi < 0 ? -1 : wi * 64 + 63 - __builtin_clzll(a[wi]);
@@ -173,17 +191,83 @@ Poly poly_mod(Poly a, const Poly &m) {
   return a;
 }
 
-Poly poly_mulmod(const Poly &a, const Poly &b, const Poly &m) { return poly_mod(poly_mul(a, b), m); }
+// a >> s (drop the s lowest coefficients)
+static Poly poly_shr(const Poly &a, int s) {
+  const int ws = s / 64, bs = s % 64;
+  if ((int)a.size() <= ws) return Poly();
+  Poly r(a.size() - ws, 0);
+  for (size_t i = 0; i < r.size(); ++i) {
+    uint64_t v = a[i + ws] >> bs;
+    if (bs && i + ws + 1 < a.size()) v |= a[i + ws + 1] << (64 - bs);
+    r[i] = v;
+  }
+  poly_trim(r);
+  return r;
+}
+
+// Barrett reduction modulo P of degree n: mu = x^(2n) div P; for deg A < 2n,
+// A div P = ((A >> n) * mu) >> n exactly over GF(2), so A mod P costs two
+// multiplications instead of n shift-xor steps.
+struct Reducer {
+  Poly P;
+  int n;
+  Poly mu;
+  explicit Reducer(const Poly &m) : P(m), n(poly_degree(m)) {
+    if (n < 1) throw std::invalid_argument("modulus must have degree >= 1");
+    // long division of x^(2n) by P, collecting the quotient
+    Poly rem((size_t)(2 * n) / 64 + 1, 0);
+    rem[(2 * n) / 64] = 1ull << ((2 * n) % 64);
+    mu.assign((size_t)n / 64 + 1, 0);
+    int dr = 2 * n;
+    while (dr >= n) {
+      const int sh = dr - n;
+      mu[sh / 64] |= 1ull << (sh % 64);
+      const int ws = sh / 64, bs = sh % 64;
+      for (size_t j = 0; j < P.size(); ++j) {
+        uint64_t v = P[j];
+        if (!v) continue;
+        rem[j + ws] ^= v << bs;
+        if (bs && j + ws + 1 < rem.size()) rem[j + ws + 1] ^= v >> (64 - bs);
+      }
+      int wi = dr / 64;
+      while (wi >= 0 && rem[wi] == 0) --wi;
+      dr = wi < 0 ? -1 : wi * 64 + 63 - __builtin_clzll(rem[wi]);
+    }
+    poly_trim(mu);
+  }
+  Poly reduce(Poly a) const {
+    if (poly_degree(a) < n) return a;
+    if (poly_degree(a) >= 2 * n) return poly_mod(std::move(a), P);
+    const Poly q = poly_shr(poly_mul(poly_shr(a, n), mu), n);
+    const Poly qp = poly_mul(q, P);
+    for (size_t i = 0; i < qp.size() && i < a.size(); ++i) a[i] ^= qp[i];
+    poly_trim(a);
+    return a;
+  }
+  Poly mulmod(const Poly &a, const Poly &b) const { return reduce(poly_mul(a, b)); }
+};
+
+Poly poly_mulmod(const Poly &a, const Poly &b, const Poly &m) { return Reducer(m).mulmod(a, b); }
+
+// squaring over GF(2) interleaves zeros between the coefficient bits
+static uint16_t g_spread[256];
+static const bool g_spread_init = [] {
+  for (int v = 0; v < 256; ++v) {
+    uint16_t r = 0;
+    for (int b = 0; b < 8; ++b) r |= (uint16_t)(((v >> b) & 1) << (2 * b));
+    g_spread[v] = r;
+  }
+  return true;
+}();
 
 static Poly poly_sqr(const Poly &a) {
-  // squaring over GF(2) interleaves zeros between the coefficient bits
   Poly r(a.size() * 2, 0);
   for (size_t i = 0; i < a.size(); ++i) {
-    uint64_t v = a[i];
+    const uint64_t v = a[i];
     uint64_t lo = 0, hi = 0;
-    for (int b = 0; b < 32; ++b) {
-      lo |= ((v >> b) & 1ull) << (2 * b);
-      hi |= ((v >> (b + 32)) & 1ull) << (2 * b);
+    for (int k = 0; k < 4; ++k) {
+      lo |= (uint64_t)g_spread[(v >> (8 * k)) & 0xFF] << (16 * k);
+      hi |= (uint64_t)g_spread[(v >> (32 + 8 * k)) & 0xFF] << (16 * k);
     }
     r[2 * i] = lo;
     r[2 * i + 1] = hi;
@@ -221,10 +305,11 @@ Poly poly_x_pow(const uint64_t *e, int ewords, const Poly &m) {
     // modulus x: x^e mod x
     return top < 0 ? r : Poly();
   }
+  const Reducer red(m);
   r = poly_mod(r, m);
   // left-to-right: square, then multiply by x for a set bit
   for (int bit = top; bit >= 0; --bit) {
-    r = poly_mod(poly_sqr(r), m);
+    r = red.reduce(poly_sqr(r));
     if ((e[bit / 64] >> (bit % 64)) & 1ull) r = poly_mulx_mod(r, m, dm);
   }
   return r;
@@ -468,6 +553,7 @@ const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64
     for (int i = 0; i < pw; ++i) plan->polys.push_back(i < (int)p.size() ? p[i] : 0);
   };
   const Poly xJ = poly_x_pow(st.data(), (int)st.size(), P);
+  const Reducer red(P);
   const uint64_t m0 = n < kDirect ? n : kDirect;
   // launch 0: x^(iJ) for i < m0
   Poly cur{1};
@@ -476,7 +562,7 @@ const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64
   for (uint64_t i = 0; i < m0; ++i) {
     direct.push_back(cur);
     push(cur);
-    cur = poly_mulmod(cur, xJ, P);
+    cur = red.mulmod(cur, xJ);
   }
   plan->launches.push_back(InitLaunch{0, m0, 0, 0, false});
   // x^(m0 J) is `cur` now
@@ -489,7 +575,7 @@ const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64
     Poly pc = xmJ;  // c = 1
     for (uint64_t c = 1; c < radix; ++c) {
       push(pc);
-      pc = poly_mulmod(pc, xmJ, P);
+      pc = red.mulmod(pc, xmJ);
     }
     // after the loop pc = x^(radix * m * J)
     uint64_t count = (radix - 1) * m;
