@@ -297,7 +297,11 @@ int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *sr
   if (!nonzero) return SLP_ERR_ZERO_STATE;
   BaseStates base;
   std::memset(&base, 0, sizeof base);
-  for (int i = 0; i < pw && i < poly_words; ++i) base.w[i] = poly[i];
+  int used = 0;
+  for (int i = 0; i < pw && i < poly_words; ++i) {
+    base.w[i] = poly[i];
+    if (poly[i]) used = i + 1;
+  }
   JumpParams p{};
   p.src = src;
   p.ld_src = ld_src;
@@ -310,6 +314,7 @@ int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *sr
   p.count = count;
   p.m = 0;
   p.batch_stride = 0;
+  p.pw_used = used;
   if (src == dst) {
     // in place: k_jump reads all words of a state before writing them
   }

@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       const uint64_t pos0 = c * CH;
       uint32_t tile = 0;
       if constexpr (MODE != FILL_POS) {
-        tile = tiles + (issued & (kFillBufs - 1)) * kTileBytes;
+        tile = tiles + (issued % kFillBufs) * kTileBytes;
         if constexpr (MODE == FILL_TMA) {
           if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
         }
@@ -712,7 +712,8 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __gri
   const uint64_t pidx = p.poly0 + (p.pmode == 1 ? t / p.m : (p.pmode == 2 ? t : 0));
   const uint64_t *poly = p.polys ? p.polys + pidx * G::pw : base.w;  // slp_jump_states: poly in params
 #pragma unroll 1
-  for (int wi = 0; wi < G::pw; ++wi) {
+  const int pw_used = p.pw_used > 0 && p.pw_used < G::pw ? p.pw_used : G::pw;
+  for (int wi = 0; wi < pw_used; ++wi) {
     const uint64_t cb = poly[wi];
 #pragma unroll
     for (int bb = 0; bb < 64; ++bb) {

@@ -43,14 +43,26 @@ struct JumpParams {
   uint64_t count;         // states per batch
   uint64_t m;             // source index t % m (0: t)
   uint64_t src_off, dst_off, batch_stride;
+  int pw_used;            // polynomial words actually used (0 = all); trims the loop for low-degree polys
 };
 
 // fill tile geometry (kernel K2): each warp emits tiles of 32 substreams x
-// kSegs x 128 bytes, one 3-D TMA store each; 7 warps x 2 buffers x 8 KiB per
-// CTA -> 2 CTAs (14 warps) per SM
-constexpr int kFillWarps = 7;
-constexpr int kSegs = 2;
-constexpr int kFillBufs = 2;
+// kSegs x 128 bytes, one 3-D TMA store each; 7 warps x 2 buffers x 16 KiB =
+// 224 KiB per CTA, one CTA (7 warps) per SM.  Chosen by an A/B sweep
+// (profiles/round1_fill_geometry.md): 512-byte row pieces beat 256-byte
+// pieces with twice the warps.
+#ifndef SLP_FILL_WARPS
+#define SLP_FILL_WARPS 7
+#endif
+#ifndef SLP_FILL_SEGS
+#define SLP_FILL_SEGS 4
+#endif
+#ifndef SLP_FILL_BUFS
+#define SLP_FILL_BUFS 2
+#endif
+constexpr int kFillWarps = SLP_FILL_WARPS;
+constexpr int kSegs = SLP_FILL_SEGS;
+constexpr int kFillBufs = SLP_FILL_BUFS;
 
 // up to 16 batches (long-jump blocks) x 16 words, passed by value
 constexpr int kMaxBaseBatches = 16;

@@ -338,3 +338,64 @@ class Substreams:
                                                _stream_ptr(self.device))
         _native.check(rc, "jump_states")
         return self
+
+
+class VecStepper:
+    """Device counterpart of the reference's numpy lane stepper
+    (engines.py:276-361): advances many states of one engine in lockstep.
+
+    ``S`` is a CUDA (k, L) tensor of native words (uint64 for w = 64, uint32
+    for w = 32) in flat word order; unlike the reference, the ring engines are
+    stored physically in flat order, so ``word(S, i)`` is ``S[i]`` and no
+    rolling offset is kept.  ``step`` runs one engine step (kernel K2 with
+    T = 1 into a scratch row); ``advance(S, steps)`` jumps by any number of
+    steps (kernel K1)."""
+
+    def __init__(self, kind, params):
+        from .generators import _TABLE
+
+        match = [s for s in _TABLE if s.kind == kind and s.params == params]
+        if not match:
+            raise ValueError("the device VecStepper supports the registry engines only")
+        self.kind = kind
+        self.params = params
+        self.spec = match[0]
+        self.off = 0
+        self._scratch = None
+
+    def _check(self, S):
+        if not isinstance(S, torch.Tensor) or not S.is_cuda:
+            raise TypeError("device VecStepper states must be a CUDA tensor (k, L)")
+        if S.dim() != 2 or S.shape[0] != self.kind.k or S.dtype != _word_dtype(self.kind.w):
+            raise ValueError(f"states must be ({self.kind.k}, L) {_word_dtype(self.kind.w)}")
+
+    def word(self, S, i: int):
+        return S[i]
+
+    def flat(self, S):
+        return S
+
+    def set_flat(self, S, flat):
+        S.copy_(flat)
+        self.off = 0
+
+    def step(self, S):
+        self._check(S)
+        L = S.shape[1]
+        if self._scratch is None or self._scratch.shape[1] < L or self._scratch.device != S.device:
+            self._scratch = torch.empty((1, L), dtype=S.dtype, device=S.device)
+        fill(self.spec, S.contiguous() if not S.is_contiguous() else S, 1, out=self._scratch[:, :L],
+             layout="position")
+
+    def advance(self, S, steps: int):
+        self._check(S)
+        if steps == 0:
+            return
+        jp = compute_jump_poly(self.spec, steps)
+        pw, pn = _native.int_to_words(jp.poly.bits)
+        ptr = ctypes.c_void_p(S.data_ptr())
+        L = S.shape[1]
+        with torch.cuda.device(S.device):
+            rc = _native.lib().slp_jump_states(native_id(self.spec), pw, pn, ptr, L, ptr, L, L,
+                                               _stream_ptr(S.device))
+        _native.check(rc, "advance")

@@ -241,3 +241,30 @@ def test_errors():
         sub.jump(P.compute_jump_poly(P.get_spec("xoroshiro128"), 5))
     with pytest.raises(ValueError):
         sub.fill(4, kind="f32")
+
+
+@pytest.mark.parametrize("name", ["xoroshiro128plus", "xoshiro256starstar", "xoshiro512plusplus",
+                                  "xoroshiro1024plus", "xorshift128plus", "xoroshiro64starstar",
+                                  "xoshiro128plusplus"])
+def test_vecstepper_matches_scalar_step(name):
+    """test_engines.py:111-136 on the device stepper: 64 steps x 5 lanes."""
+    import random
+
+    spec = P.get_spec(name)
+    kind, params = spec.kind, spec.params
+    rng = random.Random(3)
+    states = [P.bits_to_words(rng.randrange(1, 1 << kind.n), kind.k, kind.w) for _ in range(5)]
+    npdt = np.uint64 if kind.w == 64 else np.uint32
+    S = torch.from_numpy(np.array(list(zip(*states)), dtype=npdt)).cuda()
+    st = D.VecStepper(kind, params)
+    scalars = [tuple(s) for s in states]
+    for _ in range(64):
+        scalars = [P.step(kind, params, s) for s in scalars]
+        st.step(S)
+        got = S.cpu().numpy()
+        for j in range(5):
+            assert [int(st.word(got, i)[j]) for i in range(kind.k)] == list(scalars[j])
+    # advance == repeated steps
+    S2 = torch.from_numpy(np.array(list(zip(*states)), dtype=npdt)).cuda()
+    st.advance(S2, 64)
+    np.testing.assert_array_equal(S2.cpu().numpy(), S.cpu().numpy())
