@@ -579,8 +579,9 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
 #pragma unroll
     for (int j = 0; j < K; ++j) s[j] = sin[j * p.ld + stream];
     uint64_t acc_lo = 0, acc_hi = 0;  // sums of 32-bit halves (< 2^32 terms per substream)
+    uint64_t acc_lo2 = 0, acc_hi2 = 0;
     for (uint64_t c = 0; c < nfull; ++c) {
-      uint32_t lw = 0;
+      uint32_t lw = 0, lw2 = 0;
       word xx = 0;
 #pragma unroll
       for (int t = 0; t < CH; t += 2) {
@@ -588,7 +589,20 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
         G::template step_m<MSK>(s, t % K);
         const word o1 = G::template output_m<MSK>(s, (t + 1) % K);
         G::template step_m<MSK>(s, (t + 1) % K);
-#if SLP_SUM_POLICY == 1
+#if SLP_SUM_POLICY == 2
+        // separate even/odd accumulators: one IMAD.WIDE per chain per pair,
+        // nothing for ptxas to re-associate into IADD3
+        acc_lo = madw((uint32_t)o0, one, acc_lo);
+        acc_lo2 = madw((uint32_t)o1, one, acc_lo2);
+        if constexpr (G::w == 64) {
+          acc_hi = madw((uint32_t)((uint64_t)o0 >> 32), one, acc_hi);
+          acc_hi2 = madw((uint32_t)((uint64_t)o1 >> 32), one, acc_hi2);
+        }
+        if constexpr (MANT) {
+          lw = madlo((uint32_t)o0 & LOWMASK, one, lw);
+          lw2 = madlo((uint32_t)o1 & LOWMASK, one, lw2);
+        }
+#elif SLP_SUM_POLICY == 1
         acc_lo = madw((uint32_t)o0, one, acc_lo);
         acc_lo = madw((uint32_t)o1, one, acc_lo);
         if constexpr (G::w == 64) {
@@ -615,7 +629,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
         }
       }
       sx ^= (uint64_t)xx;
-      slow += lw;
+      slow += (uint64_t)lw + lw2;
     }
     for (uint64_t t = 0; t < rem; ++t) {
       const word x = G::next_flat(s);
@@ -626,6 +640,9 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
       if constexpr (F64) fs += __ull2double_rn((uint64_t)x >> SH);
     }
     // fold this substream's exact sum acc_lo + acc_hi * 2^32 into the 128-bit total
+    add128(slo, shi, acc_lo2);
+    add128(slo, shi, acc_hi2 << 32);
+    shi += acc_hi2 >> 32;
     add128(slo, shi, acc_lo);
     add128(slo, shi, acc_hi << 32);
     shi += acc_hi >> 32;
