@@ -143,6 +143,23 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
               uint64_t T, int flags, void *result, void *workspace, size_t workspace_bytes,
               void *stream);
 
+/* ---- device: Hamming-weight-dependency counting (kernel K6) -------------- */
+/* Thread i < nthreads starts from states[:, i] (the generator's single
+ * stream at test-value position c0 + i*tseg - warm, warm0 for thread 0),
+ * rebuilds the signature from `warm` test values and then, for each of the
+ * next min(tseg, total - i*tseg) test values, adds 1 to counts[sig] and its
+ * Hamming weight to sums[sig] (DEVICE arrays of 3^k uint64, accumulated).
+ * Test values are the w-bit outputs, or (split) the two 32-bit halves of
+ * each 64-bit output, low half first; transitional mode xors each value with
+ * itself shifted left by one bit, carrying the previous value's top bit.
+ * Trit: weight < lo -> 0, <= hi -> 1, else 2; signature update
+ * s <- floor(s/3) + trit * 3^(k-1).  Replaces HwdCounters._add / flush
+ * (hwd.py:206-247) fed by run_generator (hwd.py:598-621), transitional_chunks
+ * (:446-470) and split_chunks (:473-476). */
+int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, uint64_t tseg, uint64_t total,
+                  uint64_t warm, uint64_t warm0, int k, int lo, int hi, int transitional, int split,
+                  uint64_t *counts, uint64_t *sums, void *stream);
+
 /* ---- misc ---------------------------------------------------------------- */
 const char *slp_status_str(int status);
 /* last CUDA error string seen by this thread ("" if none) */

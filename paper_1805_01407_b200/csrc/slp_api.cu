@@ -390,6 +390,39 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
   return check_launch("k_fused_final");
 }
 
+int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, uint64_t tseg, uint64_t total,
+                  uint64_t warm, uint64_t warm0, int k, int lo, int hi, int transitional, int split,
+                  uint64_t *counts, uint64_t *sums, void *stream) {
+  const GenDesc *g = gen_desc(id);
+  if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
+  const GenOps *ops = gen_ops(id);
+  if (!ops) return SLP_ERR_UNSUPPORTED;
+  if (!states || !counts || !sums || k < 1 || k > 16 || ld < nthreads || tseg == 0) return SLP_ERR_INVALID;
+  if (split && g->w != 64) return SLP_ERR_INVALID;
+  if (total > nthreads * tseg || (nthreads && total <= (nthreads - 1) * tseg)) return SLP_ERR_INVALID;
+  // a CTA must not count more than 2^24 values (packed 32-bit halves of a cell)
+  if ((tseg + (warm > warm0 ? warm : warm0)) * dev::kHwdThreads > (1ull << 24) && k <= 9) return SLP_ERR_INVALID;
+  HwdParams p{};
+  p.sin = states;
+  p.ld = ld;
+  p.nthreads = nthreads;
+  p.tseg = tseg;
+  p.total = total;
+  p.warm = warm;
+  p.warm0 = warm0;
+  p.lo = lo;
+  p.hi = hi;
+  uint32_t pw = 1;
+  for (int j = 1; j < k; ++j) pw *= 3;
+  p.pow3k1 = pw;
+  p.ncells = pw * 3;
+  p.global_cells = k > 9 ? 1 : 0;
+  p.g_counts = reinterpret_cast<unsigned long long *>(counts);
+  p.g_sums = reinterpret_cast<unsigned long long *>(sums);
+  if (nthreads == 0) return SLP_OK;
+  return ops->hwd(p, transitional, split, static_cast<cudaStream_t>(stream));
+}
+
 const char *slp_build_info(void) {
   return "slp_b200 sm_100a (tcgen05-free integer path; TMA bulk tensor stores) built " __DATE__ " " __TIME__;
 }

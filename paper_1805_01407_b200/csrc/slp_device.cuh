@@ -889,6 +889,114 @@ int jump_impl(const JumpParams &p, const BaseStates *base, bool uniform, uint64_
   return check_launch("k_jump");
 }
 
+// ---- K6: Hamming-weight-dependency counting consumer ---------------------------
+//
+// Fused "generate -> test value -> popcount -> trit -> signature -> count"
+// for the HWD test (hwd.py:206-233 HwdCounters._add, :446-470 transitional,
+// :473-476 split).  Thread i owns one contiguous segment of the generator's
+// single output stream: it starts `warm` test values early (its state comes
+// from K1) only to rebuild the signature of the k preceding trits, then
+// counts `cnt` values.  Counters: one 64-bit shared-memory cell per signature
+// (count << 32 | weight sum; a CTA counts at most 2^24 values, so neither
+// half overflows), drained into 64-bit global counters once per CTA.  The
+// counts are exact, i.e. equal to the reference's large counters whenever
+// its packed small counters did not overflow (probability <= 1e-100 by its
+// batch sizing).
+
+constexpr int kHwdThreads = 256;
+constexpr uint32_t kHwdRecip = 0x55555556u;  // ceil(2^32 / 3), hwd.py:44
+
+template <class G, bool TRANS, bool SPLIT>
+__global__ void __launch_bounds__(kHwdThreads) k_hwd(HwdParams p) {
+  using word = typename G::word;
+  constexpr int K = G::k;
+  constexpr int TW = SPLIT ? 32 : G::w;  // test-value width
+  extern __shared__ unsigned long long cells[];
+  const int tid = threadIdx.x;
+  if (!p.global_cells)
+    for (uint32_t c = tid; c < p.ncells; c += kHwdThreads) cells[c] = 0ull;
+  __syncthreads();
+  const uint64_t i = (uint64_t)blockIdx.x * kHwdThreads + tid;
+  if (i < p.nthreads) {
+    const word *sin = static_cast<const word *>(p.sin);
+    word s[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) s[j] = sin[j * p.ld + i];
+    const uint64_t cnt = (i + 1) * p.tseg <= p.total ? p.tseg : p.total - i * p.tseg;
+    const uint64_t warm = i == 0 ? p.warm0 : p.warm;
+    const uint64_t nvals = warm + cnt;
+    uint32_t sig = 0;
+    uint64_t prev = 0;
+    uint64_t v = 0;  // test values produced so far
+    const int lo = p.lo, hi = p.hi;
+    const uint32_t pow3 = p.pow3k1;
+    auto consume = [&](uint64_t x) {
+      if constexpr (TRANS) {
+        const uint64_t y = x ^ (((x << 1) | (prev >> (TW - 1))) & (TW == 64 ? ~0ull : ((1ull << TW) - 1)));
+        prev = x;
+        x = y;
+      }
+      const int nu = TW == 64 ? __popcll(x) : __popc((uint32_t)x);
+      const uint32_t t = (uint32_t)(nu >= lo) + (uint32_t)(nu > hi);
+      if (v >= warm) {
+        if (p.global_cells) {
+          atomicAdd(p.g_counts + sig, 1ull);
+          atomicAdd(p.g_sums + sig, (unsigned long long)nu);
+        } else {
+          atomicAdd(cells + sig, (1ull << 32) | (unsigned long long)nu);
+        }
+      }
+      sig = (uint32_t)(((uint64_t)sig * kHwdRecip) >> 32) + t * pow3;
+      ++v;
+    };
+    while (v < nvals) {
+      const word x = G::next_flat(s);
+      if constexpr (SPLIT) {
+        consume((uint64_t)x & 0xFFFFFFFFull);
+        if (v < nvals) consume((uint64_t)x >> 32);
+      } else {
+        consume((uint64_t)x);
+      }
+    }
+  }
+  if (!p.global_cells) {
+    __syncthreads();
+    for (uint32_t c = tid; c < p.ncells; c += kHwdThreads) {
+      const unsigned long long cell = cells[c];
+      if (cell) {
+        atomicAdd(p.g_counts + c, cell >> 32);
+        atomicAdd(p.g_sums + c, cell & 0xFFFFFFFFull);
+      }
+    }
+  }
+}
+
+template <class G, bool TRANS, bool SPLIT>
+int launch_hwd_t(const HwdParams &p, cudaStream_t st) {
+  auto kern = k_hwd<G, TRANS, SPLIT>;
+  const size_t smem = p.global_cells ? 0 : (size_t)p.ncells * sizeof(unsigned long long);
+  if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                              cudaSuccess)
+    return cuda_fail("cudaFuncSetAttribute(hwd)");
+  const uint64_t grid = (p.nthreads + kHwdThreads - 1) / kHwdThreads;
+  if (grid == 0) return SLP_OK;
+  if (grid > 0x7fffffffull) return SLP_ERR_INVALID;
+  kern<<<(unsigned)grid, kHwdThreads, smem, st>>>(p);
+  return check_launch("k_hwd");
+}
+
+template <class G>
+int hwd_impl(const HwdParams &p, int transitional, int split, cudaStream_t st) {
+  if (split) {
+    if constexpr (G::w == 64) {
+      return transitional ? launch_hwd_t<G, true, true>(p, st) : launch_hwd_t<G, false, true>(p, st);
+    } else {
+      return SLP_ERR_INVALID;  // split needs 64-bit source words
+    }
+  }
+  return transitional ? launch_hwd_t<G, true, false>(p, st) : launch_hwd_t<G, false, false>(p, st);
+}
+
 template <class G>
 GenOps make_ops() {
   GenOps o;
@@ -896,6 +1004,7 @@ GenOps make_ops() {
   o.fused = &fused_impl<G>;
   o.fused_grid_cap = &fused_grid_cap<G>;
   o.jump = &jump_impl<G>;
+  o.hwd = &hwd_impl<G>;
   return o;
 }
 

@@ -70,11 +70,27 @@ struct BaseStates {
   uint64_t w[kMaxBaseBatches * 16];
 };
 
+// HWD counting consumer (kernel K6)
+struct HwdParams {
+  const void *sin;           // SoA start states, one per thread
+  uint64_t ld;
+  uint64_t nthreads;
+  uint64_t tseg;             // counted test values per thread (last thread: the rest)
+  uint64_t total;            // counted test values in this launch
+  uint64_t warm, warm0;      // warm-up test values (thread 0 may differ)
+  int lo, hi;                // trit thresholds: nu < lo -> 0, nu <= hi -> 1, else 2
+  uint32_t pow3k1;           // 3^(k-1)
+  uint32_t ncells;           // 3^k
+  int global_cells;          // 1: count straight into global memory (k > 9)
+  unsigned long long *g_counts, *g_sums;  // 3^k each, accumulated
+};
+
 struct GenOps {
   int (*fill)(const FillParams &, int out_kind, int layout, cudaStream_t);
   int (*fused)(const FusedParams &, int flags, cudaStream_t, int *grid_out);
   int (*fused_grid_cap)(int dev);
   int (*jump)(const JumpParams &, const BaseStates *, bool uniform, uint64_t nbatch, cudaStream_t);
+  int (*hwd)(const HwdParams &, int transitional, int split, cudaStream_t);
 };
 
 const GenOps *gen_ops(int id);
