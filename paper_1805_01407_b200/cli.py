@@ -5,8 +5,9 @@ arguments, output formats and exit codes (0 ok, 1 I/O, 2 usage).
 ``gen --format raw`` streams little-endian words produced on the GPU
 (LanedStream -> kernels K1/K2, cli.py:88-97 in the reference); ``hex`` and
 ``json`` print the scalar sequence (cli.py:98-104); ``jump`` prints the flat
-state after a jump (cli.py:163-180).  The reference's ``hwd`` and ``analyze``
-subcommands are outside this package's scope.
+state after a jump (cli.py:163-180); ``hwd --algo`` runs the HWD test with
+the GPU counting consumer (cli.py:122-160).  ``hwd --stdin`` and ``analyze``
+are outside this package's scope.
 
     python -m paper_1805_01407_b200 gen --algo xoshiro256starstar --seed 42 --values 1e9 > out.bin
 """
@@ -125,6 +126,37 @@ def cmd_jump(args) -> int:
     return EXIT_OK
 
 
+EXIT_STAT_FAIL = 3
+
+
+def cmd_hwd(args) -> int:
+    """HWD test of a named generator with the GPU counting consumer
+    (reference cli.py:122-160; --stdin sources are not supported here)."""
+    from . import hwd
+
+    if args.stdin or not args.algo:
+        raise CliError("this build tests generators on the GPU: use --algo NAME (no --stdin)")
+    config = hwd.HwdConfig(w=args.w, k=args.k, ell=args.ell, C=args.C, batch_size=args.batch_size,
+                           p_threshold=args.p_threshold, byte_limit=args.limit, mode=args.mode, split=args.split)
+    try:
+        report = hwd.run_generator(_get_spec(args.algo), config, seed=args.seed,
+                                   checkpoint_start=args.checkpoint_start)
+    except RuntimeError as e:
+        raise CliError(str(e), EXIT_IO)
+    if args.json:
+        print(json.dumps(report.to_dict()))
+    else:
+        print(f"mode={report.mode} w={report.w} k={report.k} ell={report.ell}")
+        for ck in report.history:
+            print(f"  {ck.bytes:>16d} bytes  p = {ck.p_value:.6g}  "
+                  f"signature {ck.faulty_signature} (category {ck.faulty_category})")
+        verdict = {"failed": "FAILED (p-value threshold tripped)", "passed": "passed to the byte limit",
+                   "inconclusive": "inconclusive (source exhausted)"}[report.status]
+        print(f"{verdict}: {report.bytes_processed} bytes, p = {report.p_value:.6g}, "
+              f"faulty signature {report.faulty_signature!r}")
+    return EXIT_STAT_FAIL if report.status == "failed" else EXIT_OK
+
+
 def build_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="paper_1805_01407_b200",
                                  description="Scrambled linear generators on B200: bulk output and jumps.")
@@ -136,6 +168,22 @@ def build_parser() -> argparse.ArgumentParser:
     g.add_argument("--values", type=_parse_count, default=16)
     g.add_argument("--format", choices=("raw", "hex", "json"), default="raw")
     g.set_defaults(func=cmd_gen)
+    h = sub.add_parser("hwd", help="run the Hamming-weight dependency test on a generator (GPU)")
+    h.add_argument("--algo")
+    h.add_argument("--stdin", action="store_true", help="not supported by this build")
+    h.add_argument("--seed", type=_parse_int, default=1)
+    h.add_argument("--w", type=int, default=64)
+    h.add_argument("--k", type=int, default=8)
+    h.add_argument("--ell", type=int, default=None)
+    h.add_argument("--C", type=int, default=None)
+    h.add_argument("--mode", choices=("standard", "transitional"), default="standard")
+    h.add_argument("--limit", type=_parse_count, default=10**15, help="byte limit")
+    h.add_argument("--p-threshold", type=float, default=1e-20, dest="p_threshold")
+    h.add_argument("--batch-size", type=_parse_count, default=None, dest="batch_size")
+    h.add_argument("--split", action="store_true", help="break 64-bit source words into two 32-bit test values")
+    h.add_argument("--checkpoint-start", type=_parse_count, default=None, dest="checkpoint_start")
+    h.add_argument("--json", action="store_true")
+    h.set_defaults(func=cmd_hwd)
     j = sub.add_parser("jump", help="print the state after a jump")
     j.add_argument("--algo", required=True)
     j.add_argument("--seed", type=_parse_int, default=0)

@@ -100,3 +100,17 @@ def test_raw_long_stream_equals_laned(monkeypatch):
 def test_raw_zero_values(monkeypatch):
     code, data = _raw(monkeypatch, "gen", "--algo", "xoshiro256plus", "--values", "0")
     assert code == 0 and data == b""
+
+
+def test_hwd_stdin_rejected(capsys):
+    code, _, err = run_cli(capsys, "hwd", "--stdin")
+    assert code == 2 and "--algo" in err
+
+
+@pytest.mark.gpu
+def test_hwd_cli_detects_xorshift128plus(capsys):
+    code, out, _ = run_cli(capsys, "hwd", "--algo", "xorshift128plus", "--mode", "transitional",
+                           "--limit", "2.4e10", "--json")
+    assert code == 3
+    doc = json.loads(out)
+    assert doc["status"] == "failed" and doc["signature"] in ("00000012", "00000021")
