@@ -245,8 +245,21 @@ def run_ours(args):
     # e2e: public API from the seed to HOST memory, every step: substream init
     # (H2D: the base state, k words) + fill + D2H of all outputs (pinned), overlapped
     e2e = None
+    host, pin_err = None, ""
     if args.e2e_steps > 0:
-        host = torch.empty((N_STREAMS, T), dtype=torch.uint64, pin_memory=True)
+        try:  # 8 GiB pinned per rank; every rank must succeed or all skip (no hang in collectives)
+            host = torch.empty((N_STREAMS, T), dtype=torch.uint64, pin_memory=True)
+        except Exception as e:  # noqa: BLE001
+            pin_err = f"pinned host buffer allocation failed: {e}"[:200]
+        ok = 1.0 if host is not None else 0.0
+        if world > 1:
+            t_ok = torch.tensor([ok], dtype=torch.float64, device=dev)
+            dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+            ok = float(t_ok.item())
+        if ok < 1.0:
+            e2e = {"error": pin_err or "pinned allocation failed on another rank"}
+            host = None
+    if host is not None:
         bufs = [torch.empty((1 << 17, T), dtype=torch.uint64, device=dev) for _ in range(2)]
         del out
         for i in range(args.e2e_steps + 1):
