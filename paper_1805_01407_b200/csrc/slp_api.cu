@@ -327,6 +327,7 @@ int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint6
   if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
   const GenOps *ops = gen_ops(id);
   if (!ops) return SLP_ERR_UNSUPPORTED;
+  if (nstreams == 0) return SLP_OK;  // nothing to generate (pointers of empty tensors may be null)
   if (!states_in || ld < nstreams || (!out && T && nstreams)) return SLP_ERR_INVALID;
   if (layout == SLP_STREAM_MAJOR && ld_out < T) return SLP_ERR_INVALID;
   if (layout == SLP_POSITION_MAJOR && ld_out < nstreams) return SLP_ERR_INVALID;

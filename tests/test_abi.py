@@ -41,7 +41,8 @@ def test_device_entry_points_reject_bad_arguments_without_touching_the_gpu():
     L = _native.lib()
     # unknown generator / null pointers are rejected before any CUDA call
     assert L.slp_fill(999, None, None, 0, 0, 0, 0, 0, None, 0, None) == _native.SLP_ERR_UNKNOWN_GENERATOR
-    assert L.slp_fill(8, None, None, 0, 0, 0, 0, 0, None, 0, None) == _native.SLP_ERR_INVALID
+    assert L.slp_fill(8, None, None, 4, 4, 4, 0, 0, None, 4, None) == _native.SLP_ERR_INVALID
+    assert L.slp_fill(8, None, None, 0, 0, 4, 0, 0, None, 4, None) == _native.SLP_OK  # nothing to do
     assert L.slp_fused(8, None, None, 0, 0, 0, 1, None, None, 0, None) == _native.SLP_ERR_INVALID
     assert L.slp_init_substreams(8, None, 1, None, 0, None, 1, 1, None) == _native.SLP_ERR_INVALID
     zero = (ctypes.c_uint64 * 4)()

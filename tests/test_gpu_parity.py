@@ -268,3 +268,75 @@ def test_vecstepper_matches_scalar_step(name):
     S2 = torch.from_numpy(np.array(list(zip(*states)), dtype=npdt)).cuda()
     st.advance(S2, 64)
     np.testing.assert_array_equal(S2.cpu().numpy(), S.cpu().numpy())
+
+
+# ---------------------------------------------------------------- edge cases
+
+
+def test_edge_empty_and_degenerate():
+    spec = P.get_spec("xoshiro256starstar")
+    sub = D.Substreams.from_seed(spec, 42, 5)
+    before = sub.states.clone()
+    out = sub.fill(0)
+    assert tuple(out.shape) == (5, 0)
+    assert torch.equal(sub.states, before)          # T = 0 leaves the states alone
+    st = torch.empty((4, 0), dtype=torch.uint64, device="cuda")
+    assert tuple(D.fill(spec, st, 16).shape) == (0, 16)   # no substreams
+    c = sub.checksum(0)
+    assert (c.sum, c.xor, c.mant, c.count) == (0, 0, 0, 0)
+    one = D.Substreams.from_seed(spec, 42, 1)        # a single substream = the scalar generator
+    g = P.Generator.from_seed(spec, 42)
+    assert [int(x) for x in one.fill(70).cpu().numpy()[0]] == [g.next() for _ in range(70)]
+
+
+def test_edge_zero_base_state_rejected():
+    spec = P.get_spec("xoshiro256plus")
+    # stride 0 is legal (every substream is the base state) ...
+    s0 = D.Substreams.from_generator(P.Generator(spec, [0, 0, 0, 1]), 4, stride=0)
+    assert all(int(x) == 1 for x in s0.states[3].cpu().numpy())
+    # ... but an all-zero base state is not (generators.py:202-203)
+    import ctypes
+
+    from paper_1805_01407_b200 import _native
+    base = (ctypes.c_uint64 * 4)(0, 0, 0, 0)
+    steps = (ctypes.c_uint64 * 1)(1)
+    buf = torch.empty((4, 4), dtype=torch.uint64, device="cuda")
+    rc = _native.lib().slp_init_substreams(6, base, 1, steps, 1, ctypes.c_void_p(buf.data_ptr()), 4, 4, None)
+    assert rc == _native.SLP_ERR_ZERO_STATE
+
+
+def test_edge_long_single_stream_and_many_blocks():
+    """One substream x 2^22 outputs (ragged vs every tile size) and 20 long-jump blocks (> one K1 batch)."""
+    spec = P.get_spec("xoroshiro128plusplus")
+    sub = D.Substreams.from_seed(spec, 3, 1)
+    T = (1 << 22) + 13
+    out = sub.fill(T).cpu().numpy()[0]
+    want = O.laned_stream("xoroshiro128plusplus", 3, T, 64, 1 << 16)
+    np.testing.assert_array_equal(out, want)
+    spec5 = P.get_spec("xoshiro512plusplus")
+    many = D.Substreams.from_seed(spec5, 42, 2, blocks=20)
+    S = many.states.cpu().numpy()
+    g = P.Generator.from_seed(spec5, 42)
+    lj = P.default_jumps(spec5)[1]
+    for b in range(20):
+        assert list(g.flat_words()) == [int(x) for x in S[:, 2 * b]], b
+        g.jump(lj)
+
+
+def test_edge_jump_identity_and_advance_matches_fill():
+    spec = P.get_spec("xoroshiro1024star")
+    a = D.Substreams.from_seed(spec, 7, 33)
+    b = D.Substreams.from_seed(spec, 7, 33)
+    a.jump(P.compute_jump_poly(spec, 0))             # x^0 = 1: identity
+    assert torch.equal(a.states, b.states)
+    a.jump(P.compute_jump_poly(spec, 1000))          # jump 1000 == emit 1000 outputs
+    b.fill(1000)
+    assert torch.equal(a.states, b.states)
+
+
+@pytest.mark.parametrize("lanes,lane_len,total", [(1, 7, 100), (3, 1, 10), (5, 1000, 12345), (64, 256, 16384)])
+def test_edge_laned_geometries(lanes, lane_len, total):
+    spec = P.get_spec("xoshiro128starstar")
+    got = np.concatenate(list(P.output_stream(spec, seed=11, total_values=total, lanes=lanes, lane_len=lane_len)))
+    g = P.Generator.from_seed(spec, 11)
+    assert [int(x) for x in got] == [g.next() for _ in range(total)]
