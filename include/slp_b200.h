@@ -123,6 +123,15 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
 int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *src, uint64_t ld_src,
                     void *dst, uint64_t ld_dst, uint64_t count, void *stream);
 
+/* seg_states[i*J + j] = states[i] * M^(j * seg_steps) for i < n, j < J:
+ * splits each of n long substreams into J consecutive segments so that a
+ * stream-major fill of the n*J segments (T = seg_steps outputs each) writes
+ * exactly the stream-major output of the n substreams with T = J*seg_steps.
+ * The B200 form of the reference's laned scheme (generators.py:426-463) for
+ * few, long substreams.  ld_seg >= n*J. */
+int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, const uint64_t *seg_steps,
+                         int seg_words, uint64_t J, void *seg_states, uint64_t ld_seg, void *stream);
+
 /* ---- device: bulk generation (kernels K2/K3/K5) ------------------------- */
 /* Emits T outputs of each of nstreams substreams (scramble current state,
  * then step: Generator.next, generators.py:244-305) into `out`, converting

@@ -76,6 +76,8 @@ SIGNATURES = {
                                            ctypes.c_uint64, ctypes.c_uint64, vp]),
     "slp_jump_states": (ctypes.c_int, [ctypes.c_int, u64p, ctypes.c_int, vp, ctypes.c_uint64, vp,
                                        ctypes.c_uint64, ctypes.c_uint64, vp]),
+    "slp_split_substreams": (ctypes.c_int, [ctypes.c_int, vp, ctypes.c_uint64, ctypes.c_uint64, u64p, ctypes.c_int,
+                                            ctypes.c_uint64, vp, ctypes.c_uint64, vp]),
     "slp_fill": (ctypes.c_int, [ctypes.c_int, vp, vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                 ctypes.c_int, ctypes.c_int, vp, ctypes.c_uint64, vp]),
     "slp_fused_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_uint64]),

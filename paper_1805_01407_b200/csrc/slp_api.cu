@@ -281,6 +281,46 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
   return SLP_OK;
 }
 
+int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, const uint64_t *seg_steps,
+                         int seg_words, uint64_t J, void *seg_states, uint64_t ld_seg, void *stream) {
+  const GenDesc *g = gen_desc(id);
+  if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
+  const GenOps *ops = gen_ops(id);
+  if (!ops) return SLP_ERR_UNSUPPORTED;
+  if (n == 0 || J == 0) return SLP_OK;
+  if (!states || !seg_states || ld < n || ld_seg < n * J || seg_words < 0 || (seg_words > 0 && !seg_steps) ||
+      J > (1ull << 20))
+    return SLP_ERR_INVALID;
+  const InitPlan *plan;
+  try {
+    plan = &segment_plan(id, seg_steps, seg_words, J);
+  } catch (const AlgebraError &e) {
+    set_last_error(e.what());
+    return SLP_ERR_ALGEBRA;
+  } catch (const std::exception &e) {
+    set_last_error(e.what());
+    return SLP_ERR_INVALID;
+  }
+  const int dev = current_device();
+  if (dev < 0) return cuda_fail("cudaGetDevice");
+  const uint64_t *d_polys = nullptr;
+  int rc = plan_polys_on_device(*plan, dev, &d_polys);
+  if (rc != SLP_OK) return rc;
+  JumpParams p{};
+  p.src = states;
+  p.ld_src = ld;
+  p.dst = seg_states;
+  p.ld_dst = ld_seg;
+  p.polys = d_polys;
+  p.poly0 = 0;
+  p.pmode = 3;  // segment (i, j) = state i jumped by x^(j*seg), i-major
+  p.use_base = 0;
+  p.count = n * J;
+  p.m = J;
+  p.batch_stride = 0;
+  return ops->jump(p, nullptr, false, 1, static_cast<cudaStream_t>(stream));
+}
+
 int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *src, uint64_t ld_src, void *dst,
                     uint64_t ld_dst, uint64_t count, void *stream) {
   const GenDesc *g = gen_desc(id);

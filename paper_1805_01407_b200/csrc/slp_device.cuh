@@ -720,16 +720,17 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __gri
     for (int j = 0; j < K; ++j) cur[j] = (word)base.w[b * K + j];
   } else {
     const word *src = static_cast<const word *>(p.src);
-    const uint64_t si = b * p.batch_stride + p.src_off + (p.m ? t % p.m : t);
+    const uint64_t si = b * p.batch_stride + p.src_off + (p.pmode == 3 ? t / p.m : (p.m ? t % p.m : t));
 #pragma unroll
     for (int j = 0; j < K; ++j) cur[j] = src[j * p.ld_src + si];
   }
 #pragma unroll
   for (int j = 0; j < K; ++j) acc[j] = 0;
-  const uint64_t pidx = p.poly0 + (p.pmode == 1 ? t / p.m : (p.pmode == 2 ? t : 0));
+  const uint64_t pidx =
+      p.poly0 + (p.pmode == 1 ? t / p.m : (p.pmode == 2 ? t : (p.pmode == 3 ? t % p.m : 0)));
   const uint64_t *poly = p.polys ? p.polys + pidx * G::pw : base.w;  // slp_jump_states: poly in params
-#pragma unroll 1
   const int pw_used = p.pw_used > 0 && p.pw_used < G::pw ? p.pw_used : G::pw;
+#pragma unroll 1
   for (int wi = 0; wi < pw_used; ++wi) {
     const uint64_t cb = poly[wi];
 #pragma unroll

@@ -38,7 +38,8 @@ struct JumpParams {
   uint64_t ld_dst;
   const uint64_t *polys;  // device, G::pw words per polynomial
   uint64_t poly0;
-  int pmode;              // 0: poly0 for all, 1: poly0 + t / m, 2: poly0 + t
+  int pmode;              // 0: poly0 for all, 1: poly0 + t / m, 2: poly0 + t,
+                          // 3: source t / m with poly0 + t % m (segment split)
   int use_base;           // source state = BaseStates entry of the batch
   uint64_t count;         // states per batch
   uint64_t m;             // source index t % m (0: t)

@@ -154,11 +154,53 @@ def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor
             raise ValueError("states_out must match states (shape, dtype, strides)")
         sout = states_out.data_ptr()
     L = _native.lib()
+    J = _split_factor(spec, n, T, layout, ld_out)
+    if J > 1:
+        wb = None if sout is None else (states if states_out is None else states_out)
+        return _fill_split(spec, gid, states, n, T, J, out, kind, wb, ld)
     with torch.cuda.device(states.device):
         rc = L.slp_fill(gid, ctypes.c_void_p(states.data_ptr()), ctypes.c_void_p(sout), ld, n, T,
                         _KIND[kind], _LAYOUT[layout], ctypes.c_void_p(out.data_ptr()), ld_out,
                         _stream_ptr(states.device))
     _native.check(rc, "fill")
+    return out
+
+
+SPLIT_TARGET_THREADS = 1 << 17
+
+
+def _split_factor(spec: GeneratorSpec, n: int, T: int, layout: str, ld_out: int) -> int:
+    """Segments per substream so that few, long substreams still fill the GPU.
+    Only for contiguous stream-major output; each segment must be long enough
+    (64 x state bits outputs) to amortise its jump."""
+    if layout != "stream" or ld_out != T or n == 0 or n >= SPLIT_TARGET_THREADS // 2:
+        return 1
+    min_seg = max(4096, 64 * spec.kind.n)
+    J = 1
+    while n * J < SPLIT_TARGET_THREADS and T % (2 * J) == 0 and T // (2 * J) >= min_seg:
+        J *= 2
+    return J
+
+
+def _fill_split(spec, gid, states, n, T, J, out, kind, sout, ld):
+    """Segment split (slp_split_substreams): substream i becomes J segments
+    i*J + j starting j*T/J steps ahead; their stream-major output with row
+    length T/J is byte-for-byte the output of the n substreams."""
+    k = spec.kind.k
+    dev = states.device
+    seg_len = T // J
+    seg = torch.empty((k, n * J), dtype=states.dtype, device=dev)
+    sw, sn = _native.int_to_words(seg_len)
+    L = _native.lib()
+    stream = _stream_ptr(dev)
+    with torch.cuda.device(dev):
+        _native.check(L.slp_split_substreams(gid, ctypes.c_void_p(states.data_ptr()), ld, n, sw, sn, J,
+                                             ctypes.c_void_p(seg.data_ptr()), n * J, stream), "split")
+        _native.check(L.slp_fill(gid, ctypes.c_void_p(seg.data_ptr()), ctypes.c_void_p(seg.data_ptr()), n * J,
+                                 n * J, seg_len, _KIND[kind], _native.STREAM_MAJOR,
+                                 ctypes.c_void_p(out.data_ptr()), seg_len, stream), "fill")
+    if sout is not None:
+        sout[:, :n].copy_(seg[:, J - 1::J])  # substream i ends where its last segment ends
     return out
 
 

@@ -340,3 +340,25 @@ def test_edge_laned_geometries(lanes, lane_len, total):
     got = np.concatenate(list(P.output_stream(spec, seed=11, total_values=total, lanes=lanes, lane_len=lane_len)))
     g = P.Generator.from_seed(spec, 11)
     assert [int(x) for x in got] == [g.next() for _ in range(total)]
+
+
+@pytest.mark.parametrize("name,n,T", [("xoshiro256starstar", 1, 1 << 20), ("xoroshiro128plus", 3, 1 << 19),
+                                      ("xoshiro128plusplus", 17, 1 << 16), ("xoroshiro1024starstar", 2, 1 << 20)])
+def test_segment_split_fill_is_transparent(name, n, T):
+    """Few, long substreams are split into jumped segments on the device; the
+    output and the advanced states must equal the unsplit computation."""
+    spec = P.get_spec(name)
+    assert D._split_factor(spec, n, T, "stream", T) > 1
+    a = D.Substreams.from_seed(spec, 5, n)
+    out = a.fill(T)
+    ref = D.Substreams.from_seed(spec, 5, n)
+    want = torch.empty_like(out)
+    L = __import__("paper_1805_01407_b200._native", fromlist=["x"])
+    import ctypes
+    rc = L.lib().slp_fill(D.native_id(spec), ctypes.c_void_p(ref.states.data_ptr()),
+                          ctypes.c_void_p(ref.states.data_ptr()), n, n, T, 0, 0,
+                          ctypes.c_void_p(want.data_ptr()), T, None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
+    assert torch.equal(a.states, ref.states)
