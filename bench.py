@@ -369,7 +369,7 @@ def run_extra(spec, dev, rank):
     c5 = {}
     for name in ("xoshiro512starstar", "xoroshiro1024plusplus"):
         s5 = P.get_spec(name)
-        sharded_checksum(s5, 42, 8, 1 << 10, 1 << 6, rank=rank, world=world, device=dev)  # warm plans
+        sharded_checksum(s5, 42, 8, 1 << 18, 1 << 4, rank=rank, world=world, device=dev)  # warm host plans
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         total, _ = sharded_checksum(s5, 42, 8, 1 << 18, 1 << 13, rank=rank, world=world, device=dev)

@@ -583,7 +583,10 @@ const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64
   };
   const Poly xJ = poly_x_pow(st.data(), (int)st.size(), P);
   const Reducer red(P);
-  const uint64_t m0 = n < kDirect ? n : kDirect;
+  // fewer direct polynomials for wide engines: each costs a host mulmod of
+  // degree-n polys (plan build time), the rounds that replace them are cheap
+  const uint64_t ndirect = g.n() <= 256 ? kDirect : (g.n() <= 512 ? kDirect / 4 : kDirect / 8);
+  const uint64_t m0 = n < ndirect ? n : ndirect;
   // launch 0: x^(iJ) for i < m0
   Poly cur{1};
   cur = poly_mod(cur, P);

@@ -204,18 +204,20 @@ def _fill_split(spec, gid, states, n, T, J, out, kind, sout, ld):
     return out
 
 
-_workspaces: dict = {}
+_ws_bytes: dict = {}
 
 
 def _workspace(gid: int, dev: torch.device) -> torch.Tensor:
+    """Per-call scratch for the per-CTA partials (tens of KB).  Allocated from
+    torch's stream-ordered caching allocator on every call, so concurrent
+    checksums on different streams never share partials."""
     key = (gid, dev.index)
-    ws = _workspaces.get(key)
-    if ws is None:
+    nbytes = _ws_bytes.get(key)
+    if nbytes is None:
         with torch.cuda.device(dev):
-            nbytes = int(_native.lib().slp_fused_workspace_bytes(gid, 0))
-        ws = torch.empty(max(nbytes, 64), dtype=torch.uint8, device=dev)
-        _workspaces[key] = ws
-    return ws
+            nbytes = max(int(_native.lib().slp_fused_workspace_bytes(gid, 0)), 64)
+        _ws_bytes[key] = nbytes
+    return torch.empty(nbytes, dtype=torch.uint8, device=dev)
 
 
 def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, exact: bool = True,
@@ -310,24 +312,30 @@ class Substreams:
 
     @classmethod
     def from_generator(cls, generator: Generator, n: int, *, stride: int | None = None, blocks: int = 1,
-                       block_stride: int | None = None, first_block: int = 0, device=None) -> "Substreams":
+                       block_stride: int | None = None, first_block: int = 0, base_offset: int = 0,
+                       device=None) -> "Substreams":
         """Substream i of block b = generator jumped by
-        (first_block + b) * block_stride + i * stride  (kernel K1)."""
+        base_offset + (first_block + b) * block_stride + i * stride  (kernel K1)."""
         spec = generator.spec
         gid = native_id(spec)
         dev = require_cuda(device)
         nbits = spec.kind.n
         stride = (1 << (nbits // 2)) if stride is None else int(stride)
         block_stride = (1 << (3 * nbits // 4)) if block_stride is None else int(block_stride)
-        if n < 1 or blocks < 1 or stride < 0 or block_stride < 0:
+        if n < 1 or blocks < 1 or stride < 0 or block_stride < 0 or base_offset < 0 or first_block < 0:
             raise ValueError("bad substream geometry")
         k = spec.kind.k
+        # block bases on the host: one jump to the first block, then one cached
+        # block_stride jump per further block (native scalar jumps, microseconds)
+        g = generator.clone()
+        off0 = base_offset + first_block * block_stride
+        if off0:
+            g.jump(compute_jump_poly(spec, off0))
+        step = compute_jump_poly(spec, block_stride) if blocks > 1 and block_stride else None
         bases = []
-        for b in range(first_block, first_block + blocks):
-            g = generator.clone()
-            off = b * block_stride
-            if off:
-                g.jump(compute_jump_poly(spec, off))
+        for b in range(blocks):
+            if b and step is not None:
+                g.jump(step)
             bases.extend(g.flat_words())
         base = (ctypes.c_uint64 * len(bases))(*bases)
         sw, sn = _native.int_to_words(stride)

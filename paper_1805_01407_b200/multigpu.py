@@ -83,12 +83,15 @@ def _device_compute(spec, seed, blocks, S, T, exact=True):
     from .device import Checksum, Substreams
     from .generators import Generator
 
-    parts = []
-    g = Generator.from_seed(spec, seed)
-    # runs of consecutive blocks are initialised together (kernel K1 handles up to 16 per launch batch)
-    for b in blocks:
-        sub = Substreams.from_generator(g, S, first_block=b)
-        parts.append(sub.checksum(T, exact=exact))
-    if not parts:
+    if not blocks:
         return Checksum(spec.kind.w, 0, 0 if exact else None, 0, 0 if exact else None, 0, None)
-    return Checksum.fold(parts)
+    g = Generator.from_seed(spec, seed)
+    lj = 1 << (3 * spec.kind.n // 4)
+    stride = blocks[1] - blocks[0] if len(blocks) > 1 else 1
+    if any(b1 - b0 != stride for b0, b1 in zip(blocks, blocks[1:])):
+        raise ValueError("blocks must be an arithmetic progression")
+    # all of this rank's blocks in one K1 init (block i = seed * M^((b0 + i*stride) * 2^(3n/4)))
+    # and ONE fused K4 launch over blocks x S substreams
+    sub = Substreams.from_generator(g, S, blocks=len(blocks), block_stride=stride * lj,
+                                    first_block=0, base_offset=blocks[0] * lj)
+    return sub.checksum(T, exact=exact)
