@@ -143,6 +143,15 @@ int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, co
 int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams,
              uint64_t T, int out_kind, int layout, void *out, uint64_t ld_out, void *stream);
 
+/* Store AND reduce in one pass: slp_fill (stream-major, TMA-eligible output)
+ * that also writes the exact checksum of the integer outputs (as slp_fused
+ * with SLP_FUSE_EXACT) to `result` (device).  BASELINE config 3 "store mode
+ * plus fused checksum".  SLP_ERR_UNSUPPORTED when the output is not
+ * TMA-addressable (then run slp_fill and slp_fused on the same states). */
+int slp_fill_checksum(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams, uint64_t T,
+                      int out_kind, void *out, uint64_t ld_out, void *result, void *workspace,
+                      size_t workspace_bytes, void *stream);
+
 /* ---- device: fused consumer (kernel K4) ---------------------------------- */
 /* Same outputs as slp_fill, reduced in-kernel instead of stored; writes one
  * slp_checksum to result (DEVICE memory).  workspace: device scratch of

@@ -395,6 +395,37 @@ int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint6
   return ops->fill(p, out_kind, layout, static_cast<cudaStream_t>(stream));
 }
 
+int slp_fill_checksum(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams, uint64_t T,
+                      int out_kind, void *out, uint64_t ld_out, void *result, void *workspace,
+                      size_t workspace_bytes, void *stream) {
+  const GenDesc *g = gen_desc(id);
+  if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
+  const GenOps *ops = gen_ops(id);
+  if (!ops) return SLP_ERR_UNSUPPORTED;
+  if (!result || !workspace) return SLP_ERR_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int grid = 0;
+  if (nstreams > 0 && T > 0) {
+    if (!states_in || !out || ld < nstreams || ld_out < T) return SLP_ERR_INVALID;
+    FillParams p{};
+    p.sin = states_in;
+    p.sout = states_out;
+    p.ld = ld;
+    p.nstreams = nstreams;
+    p.T = T;
+    p.out = out;
+    p.ld_out = ld_out;
+    p.partials = workspace;
+    p.workspace_bytes = workspace_bytes;
+    const int rc = ops->fill_csum(p, out_kind, st, &grid);
+    if (rc != SLP_OK) return rc;
+  }
+  const double fscale = g->w == 64 ? 0x1.0p-53 : 0x1.0p-24;
+  dev::k_fused_final<<<1, 256, 0, st>>>(static_cast<const slp_checksum *>(workspace), grid,
+                                        static_cast<slp_checksum *>(result), nstreams * T, fscale);
+  return check_launch("k_fused_final");
+}
+
 size_t slp_fused_workspace_bytes(int id, uint64_t nstreams) {
   (void)nstreams;
   const GenOps *ops = gen_ops(id);

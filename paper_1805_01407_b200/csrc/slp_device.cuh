@@ -414,7 +414,57 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t sr
                : "memory");
 }
 
-template <class G, int OK, int MODE>
+// CSUM: also reduce the integer outputs while storing them (wrapping sum,
+// xor, exact sum and low-bit sum, as k_fused) -- "store mode plus fused
+// checksum" of BASELINE config 3 in one pass; partials go to p.partials.
+// exact per-CTA reduction of checksum accumulators into partials[blockIdx.x]
+template <int WPB>
+__device__ __forceinline__ void reduce_checksum_block(uint64_t slo, uint64_t shi, uint64_t sx, uint64_t slow,
+                                                      double fs, void *partials) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const uint64_t olo = __shfl_xor_sync(0xffffffffu, slo, off);
+    const uint64_t ohi = __shfl_xor_sync(0xffffffffu, shi, off);
+    const uint64_t nlo = slo + olo;
+    shi = shi + ohi + (nlo < slo ? 1 : 0);
+    slo = nlo;
+    sx ^= __shfl_xor_sync(0xffffffffu, sx, off);
+    slow += __shfl_xor_sync(0xffffffffu, slow, off);
+    fs += __shfl_xor_sync(0xffffffffu, fs, off);
+  }
+  __shared__ uint64_t r_lo[WPB], r_hi[WPB], r_x[WPB], r_low[WPB];
+  __shared__ double r_fs[WPB];
+  if (lane == 0) {
+    r_lo[warp] = slo;
+    r_hi[warp] = shi;
+    r_x[warp] = sx;
+    r_low[warp] = slow;
+    r_fs[warp] = fs;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t lo = 0, hi = 0, x = 0, low = 0;
+    double f = 0.0;
+    for (int i = 0; i < WPB; ++i) {
+      const uint64_t nlo = lo + r_lo[i];
+      hi += r_hi[i] + (nlo < lo ? 1 : 0);
+      lo = nlo;
+      x ^= r_x[i];
+      low += r_low[i];
+      f += r_fs[i];
+    }
+    slp_checksum *part = static_cast<slp_checksum *>(partials) + blockIdx.x;
+    part->sum_lo = lo;
+    part->sum_hi = hi;
+    part->xor_all = x;
+    part->low_sum = low;
+    part->count = 0;
+    part->fsum = f;
+  }
+}
+
+template <class G, int OK, int MODE, bool CSUM = false>
 __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __grid_constant__ CUtensorMap tmap) {
   using word = typename G::word;
   using Cv = Out<OK, word>;
@@ -439,6 +489,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
   const uint64_t ntiles = p.T / CH;
   const uint64_t rem = p.T - ntiles * CH;
   uint32_t issued = 0;  // tiles produced by this warp
+  uint64_t cs_lo = 0, cs_hi = 0, cs_x = 0, cs_low = 0;  // CSUM accumulators (zero states emit zeros)
 
   for (uint64_t u = (uint64_t)blockIdx.x * kFillWarps + warp; u < p.nunits; u += (uint64_t)gridDim.x * kFillWarps) {
     const uint64_t row0 = u * 32;
@@ -464,8 +515,14 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
 #pragma unroll
         for (int i = 0; i < EPC; ++i) {
           const int o = (e + i) % K;
-          v[i] = Cv::conv(G::template output_m<MSK>(s, o));
+          const word r = G::template output_m<MSK>(s, o);
+          v[i] = Cv::conv(r);
           G::template step_m<MSK>(s, o);
+          if constexpr (CSUM) {
+            add128(cs_lo, cs_hi, (uint64_t)r);
+            cs_x ^= (uint64_t)r;
+            cs_low += (uint32_t)r & (G::w == 64 ? 0x7FFu : 0xFFu);
+          }
         }
         if constexpr (MODE == FILL_POS) {
           if (valid) {
@@ -518,7 +575,13 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       }
     }
     for (uint64_t t = 0; t < rem; ++t) {
-      const bits x = Cv::conv(G::next_flat(s));
+      const word r = G::next_flat(s);
+      const bits x = Cv::conv(r);
+      if constexpr (CSUM) {
+        add128(cs_lo, cs_hi, (uint64_t)r);
+        cs_x ^= (uint64_t)r;
+        cs_low += (uint32_t)r & (G::w == 64 ? 0x7FFu : 0xFFu);
+      }
       if (valid) {
         const uint64_t pos = ntiles * CH + t;
         if constexpr (MODE == FILL_POS)
@@ -535,6 +598,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
   if constexpr (MODE == FILL_TMA) {
     if (elect_one()) bulk_wait_all<0>();
   }
+  if constexpr (CSUM) reduce_checksum_block<kFillWarps>(cs_lo, cs_hi, cs_x, cs_low, 0.0, p.partials);
 }
 
 // ---- K4: fused consumer ---------------------------------------------------------
@@ -757,18 +821,19 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __gri
 
 // ---- host launchers ----------------------------------------------------------------
 
-template <class G, int OK, int MODE>
-int launch_fill(const FillParams &p0, cudaStream_t st) {
+template <class G, int OK, int MODE, bool CSUM = false>
+int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) {
   using bits = typename Out<OK, typename G::word>::bits;
   constexpr int ES = sizeof(bits);
   FillParams p = p0;
+  if (grid_out) *grid_out = 0;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof tmap);
   if constexpr (MODE == FILL_TMA) {
     int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out);
     if (rc != SLP_OK) return rc;
   }
-  auto kern = k_fill<G, OK, MODE>;
+  auto kern = k_fill<G, OK, MODE, CSUM>;
   const int smem = MODE == FILL_POS ? 0 : kFillSmem;
   p.nunits = (p.nstreams + 31) / 32;
   const int dev = current_device();
@@ -786,8 +851,37 @@ int launch_fill(const FillParams &p0, cudaStream_t st) {
   uint64_t want = (p.nunits + kFillWarps - 1) / kFillWarps;
   uint64_t cap = (uint64_t)sm_count(dev) * per_sm[dev] * fill_grid_mult();
   const unsigned grid = (unsigned)(want < cap ? want : cap);
+  if constexpr (CSUM) {
+    if ((uint64_t)grid * sizeof(slp_checksum) > p.workspace_bytes) return SLP_ERR_BUFFER;
+  }
+  if (grid_out) *grid_out = (int)grid;
   kern<<<grid, kFillThreads, smem, st>>>(p, tmap);
   return check_launch("k_fill");
+}
+
+// store + checksum in one pass: stream-major TMA path only (else UNSUPPORTED;
+// callers fall back to a fill followed by a fused pass over the same states)
+template <class G>
+int fill_csum_impl(const FillParams &p, int out_kind, cudaStream_t st, int *grid_out) {
+  constexpr int W = G::w;
+  if (grid_out) *grid_out = 0;
+  int ok;
+  if (out_kind == SLP_OUT_NATIVE || (out_kind == SLP_OUT_U64 && W == 64))
+    ok = SLP_OUT_NATIVE;
+  else if (out_kind == SLP_OUT_F64 && W == 64)
+    ok = SLP_OUT_F64;
+  else if (out_kind == SLP_OUT_F32 && W == 32)
+    ok = SLP_OUT_F32;
+  else
+    return SLP_ERR_UNSUPPORTED;
+  const int es = ok == SLP_OUT_NATIVE ? W / 8 : (ok == SLP_OUT_F32 ? 4 : 8);
+  if (!tma_ok(p.out, es, p.T, p.nstreams, p.ld_out)) return SLP_ERR_UNSUPPORTED;
+  if constexpr (W == 64) {
+    if (ok == SLP_OUT_F64) return launch_fill<G, SLP_OUT_F64, FILL_TMA, true>(p, st, grid_out);
+  } else {
+    if (ok == SLP_OUT_F32) return launch_fill<G, SLP_OUT_F32, FILL_TMA, true>(p, st, grid_out);
+  }
+  return launch_fill<G, SLP_OUT_NATIVE, FILL_TMA, true>(p, st, grid_out);
 }
 
 template <class G>
@@ -1002,6 +1096,7 @@ template <class G>
 GenOps make_ops() {
   GenOps o;
   o.fill = &fill_impl<G>;
+  o.fill_csum = &fill_csum_impl<G>;
   o.fused = &fused_impl<G>;
   o.fused_grid_cap = &fused_grid_cap<G>;
   o.jump = &jump_impl<G>;

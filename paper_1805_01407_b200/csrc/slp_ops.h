@@ -17,6 +17,8 @@ struct FillParams {
   void *out;
   uint64_t ld_out;
   uint64_t nunits;   // filled by the launcher
+  void *partials;           // store+checksum mode: slp_checksum[grid]
+  size_t workspace_bytes;
 };
 
 struct FusedParams {
@@ -88,6 +90,7 @@ struct HwdParams {
 
 struct GenOps {
   int (*fill)(const FillParams &, int out_kind, int layout, cudaStream_t);
+  int (*fill_csum)(const FillParams &, int out_kind, cudaStream_t, int *grid_out);
   int (*fused)(const FusedParams &, int flags, cudaStream_t, int *grid_out);
   int (*fused_grid_cap)(int dev);
   int (*jump)(const JumpParams &, const BaseStates *, bool uniform, uint64_t nbatch, cudaStream_t);

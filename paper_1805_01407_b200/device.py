@@ -245,6 +245,40 @@ def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, e
     return result
 
 
+def fill_checksum(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor | None = None,
+                  kind: str = "native") -> tuple[torch.Tensor, Checksum]:
+    """Store AND checksum in one pass (stream-major): returns (out, Checksum of
+    the integer outputs, exact mode).  States advance in place.  When the
+    output cannot take the TMA path, runs K4 on a copy of the states, then K2."""
+    gid = native_id(spec)
+    k = spec.kind.k
+    if states.dim() != 2 or states.shape[0] != k or not states.is_cuda or states.dtype != _word_dtype(spec.kind.w) \
+            or not states.is_contiguous():
+        raise ValueError(f"states must be a contiguous CUDA ({k}, n) {_word_dtype(spec.kind.w)} tensor")
+    n = states.shape[1]
+    dt = _out_dtype(spec, kind)
+    if out is None:
+        out = torch.empty((n, T), dtype=dt, device=states.device)
+    elif tuple(out.shape) != (n, T) or out.dtype != dt or out.stride(1) != 1 or out.device != states.device:
+        raise ValueError(f"out must be a ({n}, {T}) {dt} tensor with unit inner stride")
+    dev = states.device
+    ws = _workspace(gid, dev)
+    res = torch.empty(_native.CHECKSUM_BYTES, dtype=torch.uint8, device=dev)
+    ld_out = out.stride(0) if n > 1 else T
+    with torch.cuda.device(dev):
+        rc = _native.lib().slp_fill_checksum(gid, ctypes.c_void_p(states.data_ptr()),
+                                             ctypes.c_void_p(states.data_ptr()), n, n, T, _KIND[kind],
+                                             ctypes.c_void_p(out.data_ptr()), ld_out,
+                                             ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                             ws.numel(), _stream_ptr(dev))
+    if rc == _native.SLP_ERR_UNSUPPORTED:
+        c = fused_checksum(spec, states, T, exact=True, advance=False)
+        fill(spec, states, T, out=out, kind=kind)
+        return out, c
+    _native.check(rc, "fill_checksum")
+    return out, decode_checksum(res, spec.kind.w, True, False)
+
+
 def decode_checksum(raw: torch.Tensor | bytes, w: int, exact: bool = True, f64: bool = False) -> Checksum:
     b = bytes(raw.cpu().numpy().tobytes()) if isinstance(raw, torch.Tensor) else bytes(raw)
     return Checksum.from_raw(_native.Checksum.from_buffer_copy(b), w, exact or f64, f64)
