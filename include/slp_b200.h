@@ -173,10 +173,12 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
  * Trit: weight < lo -> 0, <= hi -> 1, else 2; signature update
  * s <- floor(s/3) + trit * 3^(k-1).  Replaces HwdCounters._add / flush
  * (hwd.py:206-247) fed by run_generator (hwd.py:598-621), transitional_chunks
- * (:446-470) and split_chunks (:473-476). */
+ * (:446-470) and split_chunks (:473-476).  The counts are exact: CTAs whose
+ * packed 32-bit shared counters fail the conservation check recount with
+ * 64-bit atomics; overflow_ctas (device, nullable) counts those CTAs. */
 int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, uint64_t tseg, uint64_t total,
                   uint64_t warm, uint64_t warm0, int k, int lo, int hi, int transitional, int split,
-                  uint64_t *counts, uint64_t *sums, void *stream);
+                  uint64_t *counts, uint64_t *sums, uint64_t *overflow_ctas, void *stream);
 
 /* ---- misc ---------------------------------------------------------------- */
 const char *slp_status_str(int status);

@@ -87,7 +87,7 @@ SIGNATURES = {
                                  ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),
     "slp_hwd_count": (ctypes.c_int, [ctypes.c_int, vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                      ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
-                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, u64p, u64p, vp]),
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, u64p, u64p, u64p, vp]),
     "slp_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "slp_last_error": (ctypes.c_char_p, []),
     "slp_build_info": (ctypes.c_char_p, []),

@@ -464,7 +464,7 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
 
 int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, uint64_t tseg, uint64_t total,
                   uint64_t warm, uint64_t warm0, int k, int lo, int hi, int transitional, int split,
-                  uint64_t *counts, uint64_t *sums, void *stream) {
+                  uint64_t *counts, uint64_t *sums, uint64_t *overflow_ctas, void *stream) {
   const GenDesc *g = gen_desc(id);
   if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
   const GenOps *ops = gen_ops(id);
@@ -472,8 +472,7 @@ int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, ui
   if (!states || !counts || !sums || k < 1 || k > 16 || ld < nthreads || tseg == 0) return SLP_ERR_INVALID;
   if (split && g->w != 64) return SLP_ERR_INVALID;
   if (total > nthreads * tseg || (nthreads && total <= (nthreads - 1) * tseg)) return SLP_ERR_INVALID;
-  // a CTA must not count more than 2^24 values (packed 32-bit halves of a cell)
-  if ((tseg + (warm > warm0 ? warm : warm0)) * dev::kHwdThreads > (1ull << 24) && k <= 9) return SLP_ERR_INVALID;
+  if (tseg >= (1ull << 32) || warm > 64 || warm0 > 64) return SLP_ERR_INVALID;
   HwdParams p{};
   p.sin = states;
   p.ld = ld;
@@ -491,6 +490,7 @@ int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, ui
   p.global_cells = k > 9 ? 1 : 0;
   p.g_counts = reinterpret_cast<unsigned long long *>(counts);
   p.g_sums = reinterpret_cast<unsigned long long *>(sums);
+  p.overflow_ctas = reinterpret_cast<unsigned long long *>(overflow_ctas);
   if (nthreads == 0) return SLP_OK;
   return ops->hwd(p, transitional, split, static_cast<cudaStream_t>(stream));
 }

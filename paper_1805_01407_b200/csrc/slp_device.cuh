@@ -991,85 +991,152 @@ int jump_impl(const JumpParams &p, const BaseStates *base, bool uniform, uint64_
 // :473-476 split).  Thread i owns one contiguous segment of the generator's
 // single output stream: it starts `warm` test values early (its state comes
 // from K1) only to rebuild the signature of the k preceding trits, then
-// counts `cnt` values.  Counters: one 64-bit shared-memory cell per signature
-// (count << 32 | weight sum; a CTA counts at most 2^24 values, so neither
-// half overflows), drained into 64-bit global counters once per CTA.  The
-// counts are exact, i.e. equal to the reference's large counters whenever
-// its packed small counters did not overflow (probability <= 1e-100 by its
-// batch sizing).
+// counts `cnt` values.
+// Counters follow the reference's packed small-counter scheme (hwd.py:167-247):
+// one 32-bit shared-memory cell per signature, count in the high 13 bits and
+// weight sum in the low 19, bumped with one 32-bit shared atomic per value
+// (the shared-atomic rate is this kernel's limit).  The host sizes segments
+// so the busiest cell expects <= 4096 counts per CTA; at the end the CTA
+// checks conservation (sum of counts == values counted, as HwdCounters.flush)
+// and drains into exact 64-bit global counters.  If a cell overflowed, the
+// CTA recounts its segments exactly with 64-bit global atomics instead, so
+// the result is always exact (the reference would report a forced failure).
 
 constexpr int kHwdThreads = 256;
 constexpr uint32_t kHwdRecip = 0x55555556u;  // ceil(2^32 / 3), hwd.py:44
 
-template <class G, bool TRANS, bool SPLIT>
-__global__ void __launch_bounds__(kHwdThreads) k_hwd(HwdParams p) {
+// counts one thread's segment; GLOBAL: 64-bit global atomics, else packed smem cells
+template <class G, bool TRANS, bool SPLIT, bool GLOBAL>
+__device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, uint32_t *cells) {
   using word = typename G::word;
   constexpr int K = G::k;
   constexpr int TW = SPLIT ? 32 : G::w;  // test-value width
-  extern __shared__ unsigned long long cells[];
-  const int tid = threadIdx.x;
-  if (!p.global_cells)
-    for (uint32_t c = tid; c < p.ncells; c += kHwdThreads) cells[c] = 0ull;
-  __syncthreads();
-  const uint64_t i = (uint64_t)blockIdx.x * kHwdThreads + tid;
-  if (i < p.nthreads) {
-    const word *sin = static_cast<const word *>(p.sin);
-    word s[K];
+  const word *sin = static_cast<const word *>(p.sin);
+  word s[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) s[j] = sin[j * p.ld + i];
-    const uint64_t cnt = (i + 1) * p.tseg <= p.total ? p.tseg : p.total - i * p.tseg;
-    const uint64_t warm = i == 0 ? p.warm0 : p.warm;
-    const uint64_t nvals = warm + cnt;
-    uint32_t sig = 0;
-    uint64_t prev = 0;
-    uint64_t v = 0;  // test values produced so far
-    const int lo = p.lo, hi = p.hi;
-    const uint32_t pow3 = p.pow3k1;
-    auto consume = [&](uint64_t x) {
-      if constexpr (TRANS) {
-        const uint64_t y = x ^ (((x << 1) | (prev >> (TW - 1))) & (TW == 64 ? ~0ull : ((1ull << TW) - 1)));
-        prev = x;
-        x = y;
-      }
-      const int nu = TW == 64 ? __popcll(x) : __popc((uint32_t)x);
-      const uint32_t t = (uint32_t)(nu >= lo) + (uint32_t)(nu > hi);
-      if (v >= warm) {
-        if (p.global_cells) {
-          atomicAdd(p.g_counts + sig, 1ull);
-          atomicAdd(p.g_sums + sig, (unsigned long long)nu);
-        } else {
-          atomicAdd(cells + sig, (1ull << 32) | (unsigned long long)nu);
-        }
-      }
-      sig = (uint32_t)(((uint64_t)sig * kHwdRecip) >> 32) + t * pow3;
-      ++v;
-    };
-    while (v < nvals) {
-      const word x = G::next_flat(s);
-      if constexpr (SPLIT) {
-        consume((uint64_t)x & 0xFFFFFFFFull);
-        if (v < nvals) consume((uint64_t)x >> 32);
+  for (int j = 0; j < K; ++j) s[j] = sin[j * p.ld + i];
+  // cnt <= tseg < 2^16 and warm <= k + 2: 32-bit counters
+  uint32_t cnt = (uint32_t)((i + 1) * p.tseg <= p.total ? p.tseg : p.total - i * p.tseg);
+  const uint32_t counted = cnt;
+  uint32_t warm = (uint32_t)(i == 0 ? p.warm0 : p.warm);
+  uint32_t sig = 0;
+  uint64_t prev = 0;
+  const int lo = p.lo, hi = p.hi;
+  const uint32_t pow3 = p.pow3k1;
+  auto consume = [&](uint64_t x, bool count) {
+    if constexpr (TRANS) {
+      const uint64_t y = x ^ (((x << 1) | (prev >> (TW - 1))) & (TW == 64 ? ~0ull : ((1ull << TW) - 1)));
+      prev = x;
+      x = y;
+    }
+    const int nu = TW == 64 ? __popcll(x) : __popc((uint32_t)x);
+    const uint32_t t = (uint32_t)(nu >= lo) + (uint32_t)(nu > hi);
+    if (count) {
+      if constexpr (GLOBAL) {
+        atomicAdd(p.g_counts + sig, 1ull);
+        atomicAdd(p.g_sums + sig, (unsigned long long)nu);
       } else {
-        consume((uint64_t)x);
+        atomicAdd(cells + sig, (1u << 19) | (uint32_t)nu);
+      }
+    }
+    sig = __umulhi(sig, kHwdRecip) + t * pow3;
+  };
+  // phase A: warm-up, only rebuilds the signature (scalar steps keep flat order)
+  bool pending = false;
+  uint64_t pend = 0;
+  while (warm > 0) {
+    const word x = G::next_flat(s);
+    if constexpr (SPLIT) {
+      consume((uint64_t)x & 0xFFFFFFFFull, false);
+      if (--warm > 0) {
+        consume((uint64_t)x >> 32, false);
+        --warm;
+      } else {
+        pending = true;  // the high half is the first counted value
+        pend = (uint64_t)x >> 32;
+      }
+    } else {
+      consume((uint64_t)x, false);
+      --warm;
+    }
+  }
+  if (pending && cnt > 0) {
+    consume(pend, true);
+    --cnt;
+  }
+  // phase B: counting in unrolled chunks of CH words (ring offsets static)
+  constexpr int CH = 16;
+  constexpr uint32_t VPW = SPLIT ? 2 : 1;  // test values per generator word
+  for (uint32_t c = cnt / (CH * VPW); c > 0; --c) {
+#pragma unroll
+    for (int t = 0; t < CH; ++t) {
+      const word x = G::output(s, t % K);
+      G::step(s, t % K);
+      if constexpr (SPLIT) {
+        consume((uint64_t)x & 0xFFFFFFFFull, true);
+        consume((uint64_t)x >> 32, true);
+      } else {
+        consume((uint64_t)x, true);
       }
     }
   }
-  if (!p.global_cells) {
-    __syncthreads();
+  cnt %= CH * VPW;
+  // phase C: tail
+  while (cnt > 0) {
+    const word x = G::next_flat(s);
+    if constexpr (SPLIT) {
+      consume((uint64_t)x & 0xFFFFFFFFull, true);
+      if (--cnt > 0) {
+        consume((uint64_t)x >> 32, true);
+        --cnt;
+      }
+    } else {
+      consume((uint64_t)x, true);
+      --cnt;
+    }
+  }
+  return counted;
+}
+
+template <class G, bool TRANS, bool SPLIT>
+__global__ void __launch_bounds__(kHwdThreads) k_hwd(HwdParams p) {
+  extern __shared__ uint32_t cells[];
+  __shared__ unsigned long long s_counted, s_cellsum;
+  const int tid = threadIdx.x;
+  const uint64_t i = (uint64_t)blockIdx.x * kHwdThreads + tid;
+  if (p.global_cells) {  // 3^k cells do not fit in shared memory (k > 9)
+    if (i < p.nthreads) hwd_segment<G, TRANS, SPLIT, true>(p, i, nullptr);
+    return;
+  }
+  for (uint32_t c = tid; c < p.ncells; c += kHwdThreads) cells[c] = 0u;
+  if (tid == 0) s_counted = s_cellsum = 0ull;
+  __syncthreads();
+  uint32_t mine = 0;
+  if (i < p.nthreads) mine = hwd_segment<G, TRANS, SPLIT, false>(p, i, cells);
+  atomicAdd(&s_counted, (unsigned long long)mine);
+  __syncthreads();
+  unsigned long long part = 0;
+  for (uint32_t c = tid; c < p.ncells; c += kHwdThreads) part += cells[c] >> 19;
+  atomicAdd(&s_cellsum, part);
+  __syncthreads();
+  if (s_cellsum == s_counted) {  // conservation holds: no packed cell overflowed
     for (uint32_t c = tid; c < p.ncells; c += kHwdThreads) {
-      const unsigned long long cell = cells[c];
+      const uint32_t cell = cells[c];
       if (cell) {
-        atomicAdd(p.g_counts + c, cell >> 32);
-        atomicAdd(p.g_sums + c, cell & 0xFFFFFFFFull);
+        atomicAdd(p.g_counts + c, (unsigned long long)(cell >> 19));
+        atomicAdd(p.g_sums + c, (unsigned long long)(cell & 0x7FFFFu));
       }
     }
+  } else {  // recount this CTA's segments exactly (rare: heavily skewed streams)
+    if (tid == 0 && p.overflow_ctas) atomicAdd(p.overflow_ctas, 1ull);
+    if (i < p.nthreads) hwd_segment<G, TRANS, SPLIT, true>(p, i, nullptr);
   }
 }
 
 template <class G, bool TRANS, bool SPLIT>
 int launch_hwd_t(const HwdParams &p, cudaStream_t st) {
   auto kern = k_hwd<G, TRANS, SPLIT>;
-  const size_t smem = p.global_cells ? 0 : (size_t)p.ncells * sizeof(unsigned long long);
+  const size_t smem = p.global_cells ? 0 : (size_t)p.ncells * sizeof(uint32_t);
   if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
                               cudaSuccess)
     return cuda_fail("cudaFuncSetAttribute(hwd)");

@@ -86,6 +86,7 @@ struct HwdParams {
   uint32_t ncells;           // 3^k
   int global_cells;          // 1: count straight into global memory (k > 9)
   unsigned long long *g_counts, *g_sums;  // 3^k each, accumulated
+  unsigned long long *overflow_ctas;      // nullable: CTAs that fell back to the exact recount
 };
 
 struct GenOps {

@@ -232,6 +232,7 @@ class _GpuCounter:
         n = 3 ** cfg.k
         self.counts = torch.zeros(n, dtype=torch.uint64, device=self.dev)
         self.sums = torch.zeros(n, dtype=torch.uint64, device=self.dev)
+        self.overflow = torch.zeros(1, dtype=torch.uint64, device=self.dev)  # CTAs recounted exactly
         self.lo = cfg.w // 2 - cfg.ell
         self.hi = cfg.w // 2 + cfg.ell
         self.dtype = torch.uint64 if spec.kind.w == 64 else torch.uint32
@@ -248,7 +249,12 @@ class _GpuCounter:
         W = k + (1 if self.trans else 0)
         if self.factor == 2:
             W += (c0 - W) & 1  # thread starts on source-word boundaries
-        tmax = (1 << 24) // 256 - W - 8
+        # packed 13-bit shared counters: keep the busiest signature (all
+        # trits central, probability pc^k) at <= 4096 expected counts per
+        # CTA of 256 segments; overflows are recounted exactly in the kernel
+        pc = central_probability(self.cfg.w, self.cfg.ell)
+        tmax = int(4096 / (256 * pc ** k)) - W
+        tmax = max(64, min(tmax, (1 << 16) - 64))
         if self.factor == 2:
             tmax -= tmax & 1
         while c0 < c1:
@@ -295,7 +301,8 @@ class _GpuCounter:
                                           c1 - c0, W, warm0, self.cfg.k, self.lo, self.hi, int(self.trans),
                                           int(self.factor == 2),
                                           ctypes.cast(self.counts.data_ptr(), _native.u64p),
-                                          ctypes.cast(self.sums.data_ptr(), _native.u64p), stream), "hwd count")
+                                          ctypes.cast(self.sums.data_ptr(), _native.u64p),
+                                          ctypes.cast(self.overflow.data_ptr(), _native.u64p), stream), "hwd count")
 
     def snapshot(self):
         return self.counts.cpu().numpy(), self.sums.cpu().numpy()
