@@ -349,3 +349,38 @@ def to_f64(values):
 def to_f32(values):
     """north_star u32 -> float: (x >> 8) * 2^-24 (no reference function; exact)"""
     return ((np.asarray(values, dtype=np.uint64) >> np.uint64(8)).astype(np.float32) * np.float32(2.0 ** -24))
+
+
+def hwd_test_values(name, seed, n_values, split=False, transitional=False, w_test=64):
+    """The first n_values HWD test values of a generator's stream:
+    hwd.py:473-476 split (low half first) then :446-470 transitional (carry 0)."""
+    factor = 2 if split else 1
+    src = laned_stream(name, seed, -(-n_values // factor), 64, 4096)
+    if split:
+        v = src.astype(np.uint64).view(np.uint32).astype(np.uint64)[:n_values]
+    else:
+        v = src[:n_values].astype(np.uint64)
+    if transitional:
+        m = np.uint64((1 << w_test) - 1) if w_test < 64 else None
+        prev = np.concatenate([np.zeros(1, np.uint64), v[:-1]])
+        sh = (v << np.uint64(1)) | (prev >> np.uint64(w_test - 1))
+        if m is not None:
+            sh &= m
+        v = v ^ sh
+    return v
+
+
+def hwd_counts(values, c0, c1, k, w_test, ell):
+    """Per-signature counts and weight sums of positions [c0, c1) of a test-value
+    array (hwd.py:206-233 HwdCounters._add, signatures from the k previous trits)."""
+    v = np.asarray(values, dtype=np.uint64)
+    nu = np.bitwise_count(v).astype(np.int64)
+    lo, hi = w_test // 2 - ell, w_test // 2 + ell
+    trits = (nu >= lo).astype(np.int64) + (nu > hi)
+    pos = np.arange(c0, c1)
+    sig = np.zeros(pos.size, dtype=np.int64)
+    for j in range(1, k + 1):
+        sig += trits[pos - j] * 3 ** (k - j)
+    counts = np.bincount(sig, minlength=3 ** k).astype(np.uint64)
+    sums = np.bincount(sig, weights=nu[pos].astype(np.float64), minlength=3 ** k).astype(np.uint64)
+    return counts, sums

@@ -304,15 +304,55 @@ class _GpuCounter:
                                           ctypes.cast(self.sums.data_ptr(), _native.u64p),
                                           ctypes.cast(self.overflow.data_ptr(), _native.u64p), stream), "hwd count")
 
+    def totals(self):
+        """(counts, sums) int64 views of the cumulative counters on the device."""
+        return self.counts.view(self.torch.int64), self.sums.view(self.torch.int64)
+
     def snapshot(self):
         return self.counts.cpu().numpy(), self.sums.cpu().numpy()
 
 
+def _global_totals(counter, group):
+    """Counters summed over all ranks (one all-reduce of the 2 x 3^k totals;
+    a plain copy on one rank), as numpy uint64 arrays."""
+    import torch
+
+    cnt, ws = counter.totals()
+    both = torch.cat([cnt, ws])
+    if group is not None:
+        import torch.distributed as dist
+
+        both = both.clone()
+        dist.all_reduce(both, op=dist.ReduceOp.SUM, group=group)
+    both = both.cpu().numpy().view(np.uint64)
+    n = cnt.numel()
+    return both[:n], both[n:]
+
+
 def run_generator(spec_or_name, config: HwdConfig, seed: int = 1, checkpoint_start: int | None = None,
-                  lanes: int = 4096, lane_len: int = 4096, device=None) -> HwdReport:
+                  lanes: int = 4096, lane_len: int = 4096, device=None, group=None,
+                  _counter_cls=None) -> HwdReport:
     """Run the HWD test on a named generator (hwd.py:598-621) with the GPU
     counting consumer.  ``lanes``/``lane_len`` only shape the reference's
-    numpy pipeline and do not change the stream; they are accepted and ignored."""
+    numpy pipeline and do not change the stream; they are accepted and ignored.
+
+    Multi-GPU: with torch.distributed initialised (or ``group`` given), every
+    checkpoint range of the stream is split into one contiguous slice per
+    rank, each rank counts its slice, and the per-signature counters are
+    summed with one all-reduce before each evaluation -- every rank then
+    evaluates the same totals and returns the same report."""
+    world, rank = 1, 0
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            world, rank = dist.get_world_size(group), dist.get_rank(group)
+            if group is None:
+                group = dist.group.WORLD
+    except ImportError:
+        pass
+    if world == 1:
+        group = None
     spec = get_spec(spec_or_name) if isinstance(spec_or_name, str) else spec_or_name
     src_w = spec.kind.w
     if config.split:
@@ -325,9 +365,15 @@ def run_generator(spec_or_name, config: HwdConfig, seed: int = 1, checkpoint_sta
     bpv = config.w // 8
     value_limit = config.byte_limit // bpv
     next_cp = checkpoint_start if checkpoint_start is not None else _checkpoint_start()
-    counter = _GpuCounter(spec, seed, config, device)
+    counter = (_counter_cls or _GpuCounter)(spec, seed, config, device)
     history: list[HwdCheckpoint] = []
     seen = 0
+
+    def count_range(a, b):
+        part = -(-(b - a) // world)  # count() accepts any start position (also mid-word in split mode)
+        ra, rb = a + rank * part, min(b, a + (rank + 1) * part)
+        if rb > ra:
+            counter.count(ra, rb)
 
     def report(status, ck):
         return HwdReport(status=status, bytes_processed=seen * bpv, values=seen,
@@ -339,11 +385,11 @@ def run_generator(spec_or_name, config: HwdConfig, seed: int = 1, checkpoint_sta
         target = min(next_cp, value_limit, stream_end)
         lo_pos = max(seen, config.k)
         if target > lo_pos:
-            counter.count(lo_pos, target)
+            count_range(lo_pos, target)
         seen = target
         at_cp, at_limit = seen >= next_cp, seen >= value_limit
         if at_cp or at_limit:
-            cnt, ws = counter.snapshot()
+            cnt, ws = _global_totals(counter, group)
             ck = evaluate_counts(cnt, ws, config, seen)
             history.append(ck)
             if at_cp:
@@ -354,7 +400,7 @@ def run_generator(spec_or_name, config: HwdConfig, seed: int = 1, checkpoint_sta
                 return report("passed", ck)
     ck = None
     if seen > config.k:
-        cnt, ws = counter.snapshot()
+        cnt, ws = _global_totals(counter, group)
         ck = evaluate_counts(cnt, ws, config, seen)
         history.append(ck)
         if ck.p_value < config.p_threshold:
