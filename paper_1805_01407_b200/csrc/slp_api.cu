@@ -81,11 +81,11 @@ int check_launch(const char *what) {
   return SLP_OK;
 }
 
-bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out) {
+bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs) {
   static int path = env_int("SLP_STORE_PATH", 0);
   if (path == 2) return false;
   const uint64_t seg = 128 / es;  // elements per 128-byte segment
-  return ((uintptr_t)out % 128) == 0 && (ld_out * es) % 16 == 0 && T >= kSegs * seg && T < (1ull << 40) &&
+  return ((uintptr_t)out % 128) == 0 && (ld_out * es) % 16 == 0 && T >= (uint64_t)segs * seg && T < (1ull << 40) &&
          nstreams < (1ull << 31) && ld_out * es < (1ull << 40) && ld_out >= T;
 }
 
@@ -104,8 +104,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // Stream-major output [nstreams][ld_out] viewed as a 3-D tensor
 // (element within a 128-byte segment, substream, segment index) so that one
-// box {128/es, 32, kSegs} is 32 substreams x kSegs contiguous segments.
-int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out) {
+// box {128/es, 32, segs} is 32 substreams x segs contiguous segments.
+int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out,
+                    int segs) {
   auto fn = encode_fn();
   if (!fn) {
     set_last_error("cuTensorMapEncodeTiled unavailable");
@@ -114,7 +115,7 @@ int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t ns
   const uint64_t seg = 128 / es;
   cuuint64_t gdim[3] = {(cuuint64_t)seg, (cuuint64_t)nstreams, (cuuint64_t)(T / seg)};
   cuuint64_t gstride[2] = {(cuuint64_t)(ld_out * es), 128};
-  cuuint32_t box[3] = {(cuuint32_t)seg, 32, (cuuint32_t)kSegs};
+  cuuint32_t box[3] = {(cuuint32_t)seg, 32, (cuuint32_t)segs};
   cuuint32_t estride[3] = {1, 1, 1};
   CUresult r = fn(map, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, out, gdim,
                   gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -168,6 +168,7 @@ struct Gen {
   static constexpr int n = K * W;
   static constexpr int pw = n / 64;  // u64 words per jump polynomial (degree < n)
   static constexpr bool ring = FAM != SLP_FAM_XOSHIRO;
+  static constexpr int sc = SC;
 
   // Rotation sites that may run on either pipe (bit set in a mask = FMA form):
   //   bit 0: engine rotation by A (xoroshiro) / by B (xoshiro)
@@ -380,17 +381,17 @@ __device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t x) {
 //
 // A warp owns 32 consecutive substreams ("unit"); lane l keeps substream
 // u*32+l in registers.  Outputs are produced in tiles of 32 substreams x
-// kTileRowBytes (= kSegs x 128 B) per substream; CH = kTileRowBytes / ES
+// row_bytes (= segs x 128 B, FillShape) per substream; CH = row_bytes / ES
 // outputs per substream per tile.  MODE:
 //   FILL_TMA     stream-major.  Every output pair goes to the warp's
 //                shared-memory tile as it is produced (STS.128,
 //                conflict-free under the 128B swizzle), and the full tile
 //                leaves with one 3-D TMA bulk tensor store
 //                (cp.async.bulk.tensor.3d, SASS UTMASTG) that writes
-//                kTileRowBytes contiguous bytes of each of the 32 rows.  The
+//                row_bytes contiguous bytes of each of the 32 rows.  The
 //                row piece is >= 256 B because HBM absorbs a column sweep of
 //                64/128-byte pieces at only ~4.5-4.8 TB/s (profiles/wpattern.cu).
-//                Two buffers per warp: store i-2 must have finished reading
+//                With B buffers per warp, store i-B must have finished reading
 //                before tile i overwrites its buffer (cp.async.bulk.wait_group.read).
 //   FILL_STAGED  stream-major, same staging, element stores (any pitch/alignment);
 //   FILL_POS     position-major: each output is one coalesced warp store.
@@ -399,9 +400,26 @@ __device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t x) {
 
 enum { FILL_TMA = 0, FILL_STAGED = 1, FILL_POS = 2 };
 constexpr int kFillThreads = kFillWarps * 32;
-constexpr int kTileRowBytes = kSegs * 128;
-constexpr int kTileBytes = 32 * kTileRowBytes;
-constexpr int kFillSmem = kFillWarps * kFillBufs * kTileBytes + 1024;
+
+// Per-generator tile shape (slp_ops.h).  The wide shape (1 KiB row pieces,
+// one buffer) wins 3-8% for every generator whose output costs little ALU
+// time; the narrow one (512 B, two buffers) keeps the store of tile i-1
+// overlapping the compute of tile i and wins for the 64-bit xoshiro ++/**
+// scramblers and xoshiro512+ (A/B over all 27, profiles/round1_fill_geometry.md).
+template <class G>
+struct FillShape {
+#if defined(SLP_FILL_SEGS) && defined(SLP_FILL_BUFS)
+  static constexpr int segs = SLP_FILL_SEGS, bufs = SLP_FILL_BUFS;
+#else
+  static constexpr bool narrow = G::w == 64 && !G::ring && (G::sc == SLP_SC_PLUSPLUS || G::sc == SLP_SC_STARSTAR ||
+                                                            (G::k == 8 && G::sc == SLP_SC_PLUS));
+  static constexpr int segs = narrow ? 4 : 8, bufs = narrow ? 2 : 1;
+#endif
+  static constexpr int row_bytes = segs * 128;
+  static constexpr int tile_bytes = 32 * row_bytes;
+  static constexpr int smem = kFillWarps * bufs * tile_bytes + 1024;
+  static_assert(smem <= 227 * 1024, "fill tiles exceed shared memory");
+};
 
 __host__ __device__ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
@@ -471,7 +489,9 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
   using bits = typename Cv::bits;
   constexpr int K = G::k;
   constexpr int ES = sizeof(bits);
-  constexpr int CH = kTileRowBytes / ES;                          // outputs per substream per tile
+  using Shape = FillShape<G>;
+  constexpr int kFillBufs = Shape::bufs, kSegs = Shape::segs, kTileBytes = Shape::tile_bytes;
+  constexpr int CH = Shape::row_bytes / ES;                       // outputs per substream per tile
   constexpr int EPC = 16 / ES;                                    // elements per 16-byte chunk
   static_assert(!G::ring || CH % K == 0, "tile must cover whole ring periods");
   constexpr int MSK = G::best_mask(0, 0);  // rotation pipe mix (ALU vs FMA), see Gen::best_mask
@@ -830,11 +850,11 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof tmap);
   if constexpr (MODE == FILL_TMA) {
-    int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out);
+    int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, FillShape<G>::segs);
     if (rc != SLP_OK) return rc;
   }
   auto kern = k_fill<G, OK, MODE, CSUM>;
-  const int smem = MODE == FILL_POS ? 0 : kFillSmem;
+  const int smem = MODE == FILL_POS ? 0 : FillShape<G>::smem;
   p.nunits = (p.nstreams + 31) / 32;
   const int dev = current_device();
   static int per_sm[64] = {0};
@@ -875,7 +895,7 @@ int fill_csum_impl(const FillParams &p, int out_kind, cudaStream_t st, int *grid
   else
     return SLP_ERR_UNSUPPORTED;
   const int es = ok == SLP_OUT_NATIVE ? W / 8 : (ok == SLP_OUT_F32 ? 4 : 8);
-  if (!tma_ok(p.out, es, p.T, p.nstreams, p.ld_out)) return SLP_ERR_UNSUPPORTED;
+  if (!tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, FillShape<G>::segs)) return SLP_ERR_UNSUPPORTED;
   if constexpr (W == 64) {
     if (ok == SLP_OUT_F64) return launch_fill<G, SLP_OUT_F64, FILL_TMA, true>(p, st, grid_out);
   } else {
@@ -903,7 +923,7 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
   if (layout == SLP_POSITION_MAJOR)
     mode = FILL_POS;
   else if (layout == SLP_STREAM_MAJOR)
-    mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out) ? FILL_TMA : FILL_STAGED;
+    mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, FillShape<G>::segs) ? FILL_TMA : FILL_STAGED;
   else
     return SLP_ERR_INVALID;
 #define SLP_FILL_CASE(OKV)                                                     \

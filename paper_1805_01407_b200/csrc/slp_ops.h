@@ -50,22 +50,18 @@ struct JumpParams {
 };
 
 // fill tile geometry (kernel K2): each warp emits tiles of 32 substreams x
-// kSegs x 128 bytes, one 3-D TMA store each; 7 warps x 2 buffers x 16 KiB =
-// 224 KiB per CTA, one CTA (7 warps) per SM.  Chosen by an A/B sweep
-// (profiles/round1_fill_geometry.md): 512-byte row pieces beat 256-byte
-// pieces with twice the warps.
+// segs x 128 bytes, one 3-D TMA store each, one CTA (7 warps) per SM.  Two
+// shapes, both 224 KiB of shared memory per CTA, chosen per generator
+// (FillShape in slp_device.cuh) by an A/B sweep over all 27
+// (profiles/round1_fill_geometry.md):
+//   narrow: 512-byte row pieces (segs 4) x 2 buffers per warp
+//   wide:   1 KiB row pieces (segs 8) x 1 buffer per warp
+// -DSLP_FILL_SEGS=.. -DSLP_FILL_BUFS=.. force one shape for every generator
+// (variant builds).
 #ifndef SLP_FILL_WARPS
 #define SLP_FILL_WARPS 7
 #endif
-#ifndef SLP_FILL_SEGS
-#define SLP_FILL_SEGS 4
-#endif
-#ifndef SLP_FILL_BUFS
-#define SLP_FILL_BUFS 2
-#endif
 constexpr int kFillWarps = SLP_FILL_WARPS;
-constexpr int kSegs = SLP_FILL_SEGS;
-constexpr int kFillBufs = SLP_FILL_BUFS;
 
 // up to 16 batches (long-jump blocks) x 16 words, passed by value
 constexpr int kMaxBaseBatches = 16;
@@ -106,7 +102,7 @@ int sm_count(int dev);
 int fill_grid_mult();
 int cuda_fail(const char *what);
 int check_launch(const char *what);
-bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out);
-int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out);
+bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);
+int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);
 
 }  // namespace slp
