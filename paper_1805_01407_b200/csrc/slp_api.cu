@@ -3,6 +3,7 @@
 // deterministic reduction of the fused consumer (K4).
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <stdexcept>
 #include <cstring>
@@ -45,14 +46,16 @@ int current_device() {
 }
 
 int sm_count(int dev) {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[64];
   if (dev < 0 || dev >= 64) return 1;
-  if (!cache[dev]) {
+  int c = cache[dev].load(std::memory_order_relaxed);
+  if (!c) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cache[dev] = v > 0 ? v : 1;
+    c = v > 0 ? v : 1;
+    cache[dev].store(c, std::memory_order_relaxed);
   }
-  return cache[dev];
+  return c;
 }
 
 static int env_int(const char *name, int dflt) {

@@ -1,7 +1,7 @@
 # A/B: run the microbenchmark against each variants/libslp_*.so
 for v in variants/libslp_*.so; do
   echo "== $v"
-  SLP_LIB=$v python profiles/microbench.py ${GENS:-xoshiro256starstar xoshiro256plusplus xoroshiro128plus xoshiro512starstar xoroshiro1024starstar xoshiro128starstar} --reps 10 2>&1 | python -c "
+  SLP_LIB=$v python profiles/microbench.py ${GENS:-xoshiro256starstar xoshiro256plusplus xoroshiro128plus xoshiro512starstar xoroshiro1024starstar xoshiro128starstar} --reps ${REPS:-10} 2>&1 | python -c "
 import json,sys
 for l in sys.stdin:
     try: d=json.loads(l)
