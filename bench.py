@@ -238,9 +238,10 @@ def run_ours(args):
                 "alg_bytes_per_unit": "8 B per u64 output + 64 B state read/write per substream per launch",
                 "kernel": "k_fill<xoshiro256**, u64, TMA>", "launch_ms": round(launch_ms, 4),
                 "frac_of_8TBps_spec": round(achieved / 8000.0, 4),
-                "frac_of_write_pattern_ceiling": round(achieved / 5985.0, 4),
-                "write_pattern_ceiling_note": "5985 GB/s = TMA-only store of the same stream-major pattern "
-                                              "(512 B row pieces, no generation), profiles/round1_write_patterns.md"}
+                "frac_of_write_pattern_ceiling": round(achieved / 6152.0, 4),
+                "write_pattern_ceiling_note": "6152 GB/s = TMA-only store of the same stream-major pattern and "
+                                              "geometry (1 KiB row pieces, 7 warps x 1 buffer, no generation), "
+                                              "profiles/round1_write_patterns.md"}
 
     # e2e: public API from the seed to HOST memory, every step: substream init
     # (H2D: the base state, k words) + fill + D2H of all outputs (pinned), overlapped
