@@ -196,6 +196,85 @@ static int plan_polys_on_device(const InitPlan &plan, int dev, const uint64_t **
   return SLP_OK;
 }
 
+// K1t jump tables of an init plan's round polynomials, per (plan, device):
+// row i of each jump matrix is unit vector i jumped by K1 (one launch over
+// the n unit vectors), then expanded into four-Russians tables on the device
+struct DevTables {
+  uint32_t *tables = nullptr;
+  uint64_t first_poly = 0, count = 0;
+};
+static std::map<std::pair<const InitPlan *, int>, DevTables> g_dev_tables;
+
+static int plan_tables_on_device(const InitPlan &plan, int id, int dev, const uint64_t *d_polys, cudaStream_t st,
+                                 const DevTables **out) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto key = std::make_pair(&plan, dev);
+  auto it = g_dev_tables.find(key);
+  if (it != g_dev_tables.end()) {
+    *out = &it->second;
+    return SLP_OK;
+  }
+  const GenDesc &g = *gen_desc(id);
+  const GenOps *ops = gen_ops(id);
+  DevTables t;
+  t.first_poly = plan.launches.size() > 1 ? plan.launches[1].poly0 : plan.polys.size() / plan.pw;
+  t.count = plan.polys.size() / plan.pw - t.first_poly;
+  if (t.count > 0) {
+    const int nb = g.n();
+    const size_t esz = g.w / 8;
+    std::vector<uint8_t> ident((size_t)g.k * nb * esz, 0);
+    for (int i = 0; i < nb; ++i) {
+      const size_t off = ((size_t)(i / g.w) * nb + i) * esz;  // SoA [k][nb]: word i / w of state i
+      const uint64_t bit = 1ull << (i % g.w);
+      std::memcpy(&ident[off], &bit, esz);
+    }
+    const uint64_t tw = ops->table_words();
+    void *d_ident = nullptr, *d_rows = nullptr;
+    if (cudaMalloc(&d_ident, ident.size()) != cudaSuccess) return cuda_fail("cudaMalloc(jump tables)");
+    if (cudaMalloc(&d_rows, ident.size()) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void **>(&t.tables), t.count * tw * sizeof(uint32_t)) != cudaSuccess) {
+      cudaFree(d_ident);
+      cudaFree(d_rows);
+      return cuda_fail("cudaMalloc(jump tables)");
+    }
+    int rc = cudaMemcpyAsync(d_ident, ident.data(), ident.size(), cudaMemcpyHostToDevice, st) == cudaSuccess
+                 ? SLP_OK
+                 : cuda_fail("cudaMemcpyAsync(identity)");
+    for (uint64_t i = 0; i < t.count && rc == SLP_OK; ++i) {
+      JumpParams p{};
+      p.src = d_ident;
+      p.ld_src = nb;
+      p.dst = d_rows;
+      p.ld_dst = nb;
+      p.polys = d_polys;
+      p.poly0 = t.first_poly + i;
+      p.pmode = 0;
+      p.count = nb;
+      rc = ops->jump(p, nullptr, true, 1, st);
+      if (rc == SLP_OK) rc = ops->build_table(d_rows, t.tables + i * tw, st);
+    }
+    if (rc == SLP_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail("jump tables");
+    cudaFree(d_ident);
+    cudaFree(d_rows);
+    if (rc != SLP_OK) {
+      cudaFree(t.tables);
+      return rc;
+    }
+  }
+  auto res = g_dev_tables.emplace(key, t);
+  *out = &res.first->second;
+  return SLP_OK;
+}
+
+// K1t replaces the uniform radix rounds of at least this many states, for
+// engines of <= 512 bits (at 1024 bits a table lookup per nibble is no
+// cheaper than the polynomial jump); SLP_INIT_TABLES=0 disables it
+static bool use_jump_tables(uint64_t count) {
+  const char *v = std::getenv("SLP_INIT_TABLES");
+  if (v && *v == '0') return false;
+  return count >= 16384;
+}
+
 }  // namespace slp
 
 using namespace slp;
@@ -263,8 +342,30 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
     rc = ops->jump(p, &base, false, nb, st);
     if (rc != SLP_OK) return rc;
   }
+  const DevTables *tabs = nullptr;
   for (size_t li = 1; li < plan->launches.size(); ++li) {
     const InitLaunch &L = plan->launches[li];
+    if (L.uniform && g->n() <= 512 && use_jump_tables(L.count * nblocks)) {
+      if (!tabs) {
+        rc = plan_tables_on_device(*plan, id, dev, d_polys, st, &tabs);
+        if (rc != SLP_OK) return rc;
+      }
+      TableJumpParams tp{};
+      tp.src = states;
+      tp.ld_src = ld;
+      tp.dst = states;
+      tp.ld_dst = ld;
+      tp.tables = tabs->tables;
+      tp.table0 = L.poly0 - tabs->first_poly;
+      tp.count = L.count;
+      tp.m = L.m;
+      tp.src_off = 0;
+      tp.dst_off = L.dst0;
+      tp.batch_stride = n;
+      rc = ops->jump_table(tp, nblocks, st);
+      if (rc != SLP_OK) return rc;
+      continue;
+    }
     JumpParams p{};
     p.src = states;
     p.ld_src = ld;

@@ -49,6 +49,19 @@ struct JumpParams {
   int pw_used;            // polynomial words actually used (0 = all); trims the loop for low-degree polys
 };
 
+// table-driven uniform jump (kernel K1t): dst[dst_off + t] = src[src_off + t % m]
+// jumped by table (table0 + t / m), t < count; tables from build_table
+struct TableJumpParams {
+  const void *src;
+  uint64_t ld_src;
+  void *dst;
+  uint64_t ld_dst;
+  const uint32_t *tables;  // device, table_words() uint32 per table
+  uint64_t table0;
+  uint64_t count, m;
+  uint64_t src_off, dst_off, batch_stride;
+};
+
 // fill tile geometry (kernel K2): each warp emits tiles of 32 substreams x
 // segs x 128 bytes, one 3-D TMA store each, one CTA (7 warps) per SM.  Two
 // shapes, both 224 KiB of shared memory per CTA, chosen per generator
@@ -92,6 +105,11 @@ struct GenOps {
   int (*fused_grid_cap)(int dev);
   int (*jump)(const JumpParams &, const BaseStates *, bool uniform, uint64_t nbatch, cudaStream_t);
   int (*hwd)(const HwdParams &, int transitional, int split, cudaStream_t);
+  // K1t: uint32 words per jump table; expand the n rows of a jump matrix
+  // (SoA [k][n] states: row i = unit vector i jumped) into one table
+  uint64_t (*table_words)();
+  int (*build_table)(const void *rows, uint32_t *table, cudaStream_t);
+  int (*jump_table)(const TableJumpParams &, uint64_t nbatch, cudaStream_t);
 };
 
 const GenOps *gen_ops(int id);
