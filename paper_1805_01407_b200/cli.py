@@ -81,9 +81,9 @@ def write_raw(spec: GeneratorSpec, gen: Generator, n: int, out) -> None:
     lanes = max(1, min(_RAW_MAX_LANES, -(-n // _RAW_LANE_LEN)))
     stream = generators.LanedStream(spec, generator=gen, lanes=lanes, lane_len=_RAW_LANE_LEN)
     dtype = np.dtype("<u8") if spec.kind.w == 64 else np.dtype("<u4")
-    for chunk in stream.chunks(n, device=True, native=True):
-        host = chunk.cpu().numpy()
-        out.write(host.astype(dtype, copy=False).tobytes())
+    # pipelined GPU -> pinned staging -> output, no intermediate copies
+    for chunk in stream.chunks(n, native=True, _views=True):
+        out.write(memoryview(chunk.astype(dtype, copy=False)).cast("B"))
 
 
 def cmd_gen(args) -> int:

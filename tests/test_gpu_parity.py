@@ -362,3 +362,20 @@ def test_segment_split_fill_is_transparent(name, n, T):
     torch.cuda.synchronize()
     assert torch.equal(out, want)
     assert torch.equal(a.states, ref.states)
+
+
+def test_host_chunks_are_fresh_and_match_device_chunks():
+    """Pipelined host delivery (staging double buffer + threaded copies) yields
+    caller-owned arrays equal to the device chunks (generators.py:482)."""
+    spec = P.get_spec("xoshiro256plusplus")
+    total = 5 * 512 * 4096 + 777  # 5 full superbatches + a ragged tail
+    host = list(P.LanedStream(spec, seed=9, lanes=512, lane_len=4096).chunks(total))
+    dev = [c.cpu().numpy() for c in P.LanedStream(spec, seed=9, lanes=512, lane_len=4096).chunks(total, device=True)]
+    assert [h.size for h in host] == [d.size for d in dev]
+    for h, d in zip(host, dev):
+        assert np.array_equal(h, d)
+    for a in range(len(host)):
+        for b in range(a + 1, len(host)):
+            assert not np.shares_memory(host[a], host[b])
+    host[0][:] = 0  # caller owns it: later chunks are unaffected
+    assert np.array_equal(host[1], dev[1])
