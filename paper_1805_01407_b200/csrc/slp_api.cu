@@ -266,9 +266,8 @@ static int plan_tables_on_device(const InitPlan &plan, int id, int dev, const ui
   return SLP_OK;
 }
 
-// K1t replaces the uniform radix rounds of at least this many states, for
-// engines of <= 512 bits (at 1024 bits a table lookup per nibble is no
-// cheaper than the polynomial jump); SLP_INIT_TABLES=0 disables it
+// K1t replaces the uniform radix rounds of at least this many states
+// (SLP_INIT_TABLES=0 disables it)
 static bool use_jump_tables(uint64_t count) {
   const char *v = std::getenv("SLP_INIT_TABLES");
   if (v && *v == '0') return false;
@@ -345,7 +344,7 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
   const DevTables *tabs = nullptr;
   for (size_t li = 1; li < plan->launches.size(); ++li) {
     const InitLaunch &L = plan->launches[li];
-    if (L.uniform && g->n() <= 512 && use_jump_tables(L.count * nblocks)) {
+    if (L.uniform && use_jump_tables(L.count * nblocks)) {
       if (!tabs) {
         rc = plan_tables_on_device(*plan, id, dev, d_polys, st, &tabs);
         if (rc != SLP_OK) return rc;
