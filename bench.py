@@ -138,6 +138,14 @@ def ncu_traffic(kernel_tag):
         return None
 
 
+def fused_pipes():
+    try:
+        with open(os.path.join(ROOT, "profiles", "round1_fused_pipes.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
 def cpu_baseline(steps_budget_s=20.0):
     from oracle.cpu_baseline import CpuBaseline
 
@@ -369,6 +377,17 @@ def run_extra(spec, dev, rank):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         res[label] = {"outputs_per_s": N_STREAMS * T / (ms / 1e3), "ms_per_step": ms}
+        # INT roofline of K4: ALU-pipe SASS per output (committed ncu pipe counts)
+        # x outputs/s against the measured ALU-pipe peak (profiles/int_peak.cu)
+        pipes = fused_pipes().get({"fused_int": "sum_xor", "fused_exact": "exact",
+                                   "fused_exact_f64": "exact_f64"}[label])
+        if pipes:
+            peak = fused_pipes()["int_peaks"]["alu_warp_inst_per_s"]
+            ach = res[label]["outputs_per_s"] * pipes["alu_sass_per_output"] / 32
+            res[label]["roofline"] = {"bound": "int (ALU pipe)", "achieved": ach, "peak": peak,
+                                      "unit": "warp-inst/s", "frac": round(ach / peak, 4),
+                                      "alu_sass_per_output": round(pipes["alu_sass_per_output"], 3),
+                                      "source": "profiles/round1_fused_pipes.json"}
     # config 5 whole job: 2^34 outputs = 8 long-jump blocks x 2^18 substreams x 2^13,
     # blocks b == rank (mod world), fused exact checksum per GPU, one all_gather
     import torch.distributed as dist

@@ -1,0 +1,78 @@
+// Measured integer-pipe peaks on this B200 (the INT roofline of kernel K4):
+// long dependency-free streams of LOP3 (ALU pipe), SHF.L.W (ALU pipe) and
+// IMAD (FMA pipe), and an ALU+FMA mix, all SMs, CUDA events.
+// Reports warp-instructions per second per GPU and per SM per cycle.
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a profiles/int_peak.cu -o /tmp/int_peak
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int CH = 8;       // independent chains per thread
+constexpr int ITERS = 4096;
+
+template <int OP>
+__global__ void k(uint32_t *out, uint32_t seed) {
+  uint32_t a[CH], b[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    a[c] = seed + threadIdx.x * 7 + c;
+    b[c] = seed ^ (c * 0x9E3779B9u);
+  }
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (OP == 0) {  // LOP3: 3-input xor
+        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[c]) : "r"(b[c]), "r"(i));
+      } else if (OP == 1) {  // funnel shift (rotate)
+        asm volatile("shf.l.wrap.b32 %0, %0, %1, 13;" : "+r"(a[c]) : "r"(b[c]));
+      } else if (OP == 2) {  // IMAD
+        asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[c]) : "r"(b[c]), "r"(i));
+      } else {  // ALU + FMA interleaved
+        if (c & 1)
+          asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[c]) : "r"(b[c]), "r"(i));
+        else
+          asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[c]) : "r"(b[c]), "r"(i));
+      }
+    }
+  }
+  uint32_t r = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) r ^= a[c];
+  if (r == 0x12345678u) out[0] = r;
+}
+
+int main() {
+  int sms, clk;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  uint32_t *out;
+  cudaMalloc(&out, 4);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const char *names[] = {"LOP3 (ALU)", "SHF.L.W (ALU)", "IMAD (FMA)", "LOP3+IMAD mix"};
+  auto run = [&](int op, auto kern) {
+    const int grid = sms * 8, block = 256;
+    kern<<<grid, block>>>(out, 1);
+    cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0);
+      kern<<<grid, block>>>(out, 1);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = ms < best ? ms : best;
+    }
+    const double winst = (double)grid * block / 32 * ITERS * CH;
+    const double per_s = winst / (best / 1e3);
+    printf("{\"op\": \"%s\", \"warp_inst_per_s\": %.4g, \"per_sm_per_cycle_at_max_clock\": %.3f}\n", names[op], per_s,
+           per_s / sms / (clk * 1e3));
+  };
+  run(0, k<0>);
+  run(1, k<1>);
+  run(2, k<2>);
+  run(3, k<3>);
+  return 0;
+}
