@@ -1,0 +1,85 @@
+"""Every fill kind of every generator against the oracle.  The tile
+configuration of kernel K2 is chosen per (generator, kind) from a measured
+table (csrc/slp_fill_tuning.h), so each combination is its own code path:
+store native, store converted (u64 zero-extension / f64 / f32), store +
+checksum in one pass.  Sizes exercise several tiles, the rolled sub-block
+loop, the pre-wait chunks, the per-lane tail and warps that process more
+than one unit of 32 substreams (next-unit state prefetch)."""
+
+import numpy as np
+import pytest
+
+import paper_1805_01407_b200 as P
+from paper_1805_01407_b200 import device as D
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ALL = P.registry_names(include_analysis=True)
+
+
+def _flat(spec, L, seed):
+    rng = np.random.default_rng(seed)
+    flat = rng.integers(0, 1 << 63, size=(spec.kind.k, L), dtype=np.uint64) | np.uint64(1)
+    if spec.kind.w == 32:
+        flat &= np.uint64(0xFFFFFFFF)
+    return flat
+
+
+def _kinds(w):
+    return ["native", "f64"] if w == 64 else ["native", "u64", "f32"]
+
+
+def _convert(ints, kind, w):
+    if kind == "native":
+        return ints
+    if kind == "u64":
+        return ints.astype(np.uint64)
+    return O.to_f64(ints) if kind == "f64" else O.to_f32(ints)
+
+
+def _bits(a):
+    return a.view(np.uint64) if a.dtype in (np.float64, np.uint64) else a.view(np.uint32)
+
+
+@pytest.mark.parametrize("name", ALL)
+@pytest.mark.parametrize("T", [1000, 2061])
+def test_all_kinds_vs_oracle(name, T):
+    spec = P.get_spec(name)
+    w = spec.kind.w
+    flat = _flat(spec, 45, T)
+    want, want_S = O.vec_outputs(name, flat, T)
+    want = want.astype(np.uint64 if w == 64 else np.uint32)
+    oc = O.checksum(want, w)
+    for kind in _kinds(w):
+        exp = _convert(want, kind, w)
+        sub = D.Substreams.from_states(spec, flat)
+        got = sub.fill(T, kind=kind).cpu().numpy()
+        np.testing.assert_array_equal(_bits(got), _bits(exp), err_msg=f"{name} {kind}")
+        np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
+        if kind in ("native", "f64", "f32"):
+            sub = D.Substreams.from_states(spec, flat)
+            out, c = D.fill_checksum(spec, sub.states, T, kind=kind)
+            np.testing.assert_array_equal(_bits(out.cpu().numpy()), _bits(exp), err_msg=f"{name} csum {kind}")
+            assert (c.sum, c.xor, c.mant) == (oc["sum"], oc["xor"], oc["mant"]), (name, kind)
+            np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
+
+
+@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro128plus", "xoroshiro1024plusplus",
+                                  "xoshiro512plusplus", "xoshiro128starstar", "xoroshiro64starstar"])
+def test_many_units_per_warp(name):
+    """More 32-substream units than resident warps (148 SMs x 7 warps), ragged."""
+    spec = P.get_spec(name)
+    w = spec.kind.w
+    L, T = 148 * 7 * 32 * 2 + 5, 300
+    flat = _flat(spec, L, 11)
+    want, want_S = O.vec_outputs(name, flat, T)
+    want = want.astype(np.uint64 if w == 64 else np.uint32)
+    sub = D.Substreams.from_states(spec, flat)
+    got = sub.fill(T).cpu().numpy()
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
+    sub = D.Substreams.from_states(spec, flat)
+    _, c = D.fill_checksum(spec, sub.states, T)
+    oc = O.checksum(want, w)
+    assert (c.sum, c.xor, c.mant) == (oc["sum"], oc["xor"], oc["mant"])
