@@ -10,6 +10,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "slp_device.cuh"
@@ -205,6 +206,62 @@ struct DevTables {
 };
 static std::map<std::pair<const InitPlan *, int>, DevTables> g_dev_tables;
 
+// builds `count` K1t tables on `st` (synchronised before returning): table i
+// from polynomial i of the device array `d_polys` (or, when d_polys is null,
+// from the single host polynomial `host_poly` passed as a kernel parameter)
+static int build_jump_tables(int id, const uint64_t *d_polys, uint64_t first_poly, const uint64_t *host_poly,
+                             uint64_t count, cudaStream_t st, uint32_t **out) {
+  const GenDesc &g = *gen_desc(id);
+  const GenOps *ops = gen_ops(id);
+  const int nb = g.n();
+  const size_t esz = g.w / 8;
+  std::vector<uint8_t> ident((size_t)g.k * nb * esz, 0);
+  for (int i = 0; i < nb; ++i) {
+    const size_t off = ((size_t)(i / g.w) * nb + i) * esz;  // SoA [k][nb]: word i / w of state i
+    const uint64_t bit = 1ull << (i % g.w);
+    std::memcpy(&ident[off], &bit, esz);
+  }
+  const uint64_t tw = ops->table_words();
+  void *d_ident = nullptr, *d_rows = nullptr;
+  uint32_t *tables = nullptr;
+  if (cudaMalloc(&d_ident, ident.size()) != cudaSuccess) return cuda_fail("cudaMalloc(jump tables)");
+  if (cudaMalloc(&d_rows, ident.size()) != cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void **>(&tables), count * tw * sizeof(uint32_t)) != cudaSuccess) {
+    cudaFree(d_ident);
+    cudaFree(d_rows);
+    return cuda_fail("cudaMalloc(jump tables)");
+  }
+  int rc = cudaMemcpyAsync(d_ident, ident.data(), ident.size(), cudaMemcpyHostToDevice, st) == cudaSuccess
+               ? SLP_OK
+               : cuda_fail("cudaMemcpyAsync(identity)");
+  BaseStates base;
+  std::memset(&base, 0, sizeof base);
+  if (host_poly)
+    for (int i = 0; i < g.n() / 64; ++i) base.w[i] = host_poly[i];
+  for (uint64_t i = 0; i < count && rc == SLP_OK; ++i) {
+    JumpParams p{};
+    p.src = d_ident;
+    p.ld_src = nb;
+    p.dst = d_rows;
+    p.ld_dst = nb;
+    p.polys = d_polys;  // null: the polynomial is in the BaseStates parameter block
+    p.poly0 = first_poly + i;
+    p.pmode = 0;
+    p.count = nb;
+    rc = ops->jump(p, host_poly ? &base : nullptr, true, 1, st);
+    if (rc == SLP_OK) rc = ops->build_table(d_rows, tables + i * tw, st);
+  }
+  if (rc == SLP_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail("jump tables");
+  cudaFree(d_ident);
+  cudaFree(d_rows);
+  if (rc != SLP_OK) {
+    cudaFree(tables);
+    return rc;
+  }
+  *out = tables;
+  return SLP_OK;
+}
+
 static int plan_tables_on_device(const InitPlan &plan, int id, int dev, const uint64_t *d_polys, cudaStream_t st,
                                  const DevTables **out) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -214,60 +271,54 @@ static int plan_tables_on_device(const InitPlan &plan, int id, int dev, const ui
     *out = &it->second;
     return SLP_OK;
   }
-  const GenDesc &g = *gen_desc(id);
-  const GenOps *ops = gen_ops(id);
   DevTables t;
   t.first_poly = plan.launches.size() > 1 ? plan.launches[1].poly0 : plan.polys.size() / plan.pw;
   t.count = plan.polys.size() / plan.pw - t.first_poly;
   if (t.count > 0) {
-    const int nb = g.n();
-    const size_t esz = g.w / 8;
-    std::vector<uint8_t> ident((size_t)g.k * nb * esz, 0);
-    for (int i = 0; i < nb; ++i) {
-      const size_t off = ((size_t)(i / g.w) * nb + i) * esz;  // SoA [k][nb]: word i / w of state i
-      const uint64_t bit = 1ull << (i % g.w);
-      std::memcpy(&ident[off], &bit, esz);
-    }
-    const uint64_t tw = ops->table_words();
-    void *d_ident = nullptr, *d_rows = nullptr;
-    if (cudaMalloc(&d_ident, ident.size()) != cudaSuccess) return cuda_fail("cudaMalloc(jump tables)");
-    if (cudaMalloc(&d_rows, ident.size()) != cudaSuccess ||
-        cudaMalloc(reinterpret_cast<void **>(&t.tables), t.count * tw * sizeof(uint32_t)) != cudaSuccess) {
-      cudaFree(d_ident);
-      cudaFree(d_rows);
-      return cuda_fail("cudaMalloc(jump tables)");
-    }
-    int rc = cudaMemcpyAsync(d_ident, ident.data(), ident.size(), cudaMemcpyHostToDevice, st) == cudaSuccess
-                 ? SLP_OK
-                 : cuda_fail("cudaMemcpyAsync(identity)");
-    for (uint64_t i = 0; i < t.count && rc == SLP_OK; ++i) {
-      JumpParams p{};
-      p.src = d_ident;
-      p.ld_src = nb;
-      p.dst = d_rows;
-      p.ld_dst = nb;
-      p.polys = d_polys;
-      p.poly0 = t.first_poly + i;
-      p.pmode = 0;
-      p.count = nb;
-      rc = ops->jump(p, nullptr, true, 1, st);
-      if (rc == SLP_OK) rc = ops->build_table(d_rows, t.tables + i * tw, st);
-    }
-    if (rc == SLP_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail("jump tables");
-    cudaFree(d_ident);
-    cudaFree(d_rows);
-    if (rc != SLP_OK) {
-      cudaFree(t.tables);
-      return rc;
-    }
+    const int rc = build_jump_tables(id, d_polys, t.first_poly, nullptr, t.count, st, &t.tables);
+    if (rc != SLP_OK) return rc;
   }
   auto res = g_dev_tables.emplace(key, t);
   *out = &res.first->second;
   return SLP_OK;
 }
 
+// K1t tables of single jump polynomials (slp_jump_states), per (engine,
+// device, polynomial); at most kMaxPolyTables per device, never evicted
+// (a table may be in use on any stream), K1 once the cache is full
+constexpr size_t kMaxPolyTables = 32;
+static std::map<std::tuple<int, int, std::vector<uint64_t>>, uint32_t *> g_poly_tables;
+static std::map<int, size_t> g_poly_tables_per_dev;
+
+static int poly_table_on_device(int id, int dev, const uint64_t *poly, cudaStream_t st, const uint32_t **out) {
+  const GenDesc &g = *gen_desc(id);
+  std::vector<uint64_t> pv(poly, poly + g.n() / 64);
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto key = std::make_tuple(engine_id(id), dev, pv);
+  auto it = g_poly_tables.find(key);
+  if (it != g_poly_tables.end()) {
+    *out = it->second;
+    return SLP_OK;
+  }
+  if (g_poly_tables_per_dev[dev] >= kMaxPolyTables) {
+    *out = nullptr;
+    return SLP_OK;
+  }
+  uint32_t *t = nullptr;
+  const int rc = build_jump_tables(id, nullptr, 0, pv.data(), 1, st, &t);
+  if (rc != SLP_OK) return rc;
+  g_poly_tables[key] = t;
+  ++g_poly_tables_per_dev[dev];
+  *out = t;
+  return SLP_OK;
+}
+
 // K1t replaces the uniform radix rounds of at least this many states
 // (SLP_INIT_TABLES=0 disables it)
+// slp_jump_states: K1t from this many states on (a table costs ~n unit-vector
+// jumps to build, then is cached per polynomial)
+constexpr uint64_t kJumpTableMinStates = 65536;
+
 static bool use_jump_tables(uint64_t count) {
   const char *v = std::getenv("SLP_INIT_TABLES");
   if (v && *v == '0') return false;
@@ -459,10 +510,31 @@ int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *sr
   p.m = 0;
   p.batch_stride = 0;
   p.pw_used = used;
-  if (src == dst) {
-    // in place: k_jump reads all words of a state before writing them
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // many states: K1t with a cached table of this polynomial.  In place only
+  // for n <= 256 (one table slice: a thread reads its whole state before
+  // writing it); wider engines split the output words over CTAs, which would
+  // race with the reads of the other slices.
+  if (count >= kJumpTableMinStates && (src != dst || g->n() <= 256) && use_jump_tables(count)) {
+    const int dev = current_device();
+    if (dev < 0) return cuda_fail("cudaGetDevice");
+    const uint32_t *table = nullptr;
+    const int rc = poly_table_on_device(id, dev, base.w, st, &table);
+    if (rc != SLP_OK) return rc;
+    if (table) {
+      TableJumpParams tp{};
+      tp.src = src;
+      tp.ld_src = ld_src;
+      tp.dst = dst;
+      tp.ld_dst = ld_dst;
+      tp.tables = table;
+      tp.table0 = 0;
+      tp.count = count;
+      tp.m = count;
+      return ops->jump_table(tp, 1, st);
+    }
   }
-  return ops->jump(p, &base, true, 1, static_cast<cudaStream_t>(stream));
+  return ops->jump(p, &base, true, 1, st);
 }
 
 int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams, uint64_t T,

@@ -417,8 +417,18 @@ class Substreams:
             raise ValueError("jump polynomial is zero")
         pw, pn = _native.int_to_words(jp.poly.bits)
         ptr = ctypes.c_void_p(self.states.data_ptr())
+        ld = self.states.stride(0)
         with torch.cuda.device(self.device):
-            rc = _native.lib().slp_jump_states(self.gid, pw, pn, ptr, self.count, ptr, self.count, self.count,
+            if self.spec.kind.n > 256 and self.count >= (1 << 16):
+                # out of place, so the table-driven kernel K1t can run (its
+                # wide-engine slices cannot update in place), then copy back
+                tmp = torch.empty((self.spec.kind.k, self.count), dtype=self.states.dtype, device=self.device)
+                rc = _native.lib().slp_jump_states(self.gid, pw, pn, ptr, ld, ctypes.c_void_p(tmp.data_ptr()),
+                                                   self.count, self.count, _stream_ptr(self.device))
+                _native.check(rc, "jump_states")
+                self.states[:, : self.count].copy_(tmp)
+                return self
+            rc = _native.lib().slp_jump_states(self.gid, pw, pn, ptr, ld, ptr, ld, self.count,
                                                _stream_ptr(self.device))
         _native.check(rc, "jump_states")
         return self

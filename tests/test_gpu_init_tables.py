@@ -55,3 +55,35 @@ def test_tables_match_host_jumps(name):
             if i:
                 g.jump(P.compute_jump_poly(spec, i << (nb // 2)))
             assert list(g.flat_words()) == [int(v) for v in S[:, b * n + i]], (b, i)
+
+
+@pytest.mark.parametrize("name", ENGINES)
+def test_jump_states_tables_equal_polynomial(name):
+    """slp_jump_states on >= 65536 states uses K1t with a cached table (in
+    place for n <= 256, out of place above); equal to K1."""
+    spec = P.get_spec(name)
+    jp = P.compute_jump_poly(spec, 987654321987654321)
+    base = D.Substreams.from_seed(spec, 5, 70000)
+    res = {}
+    for flag in ("1", "0"):
+        old = os.environ.get("SLP_INIT_TABLES")
+        os.environ["SLP_INIT_TABLES"] = flag
+        try:
+            sub = D.Substreams(spec, base.states.clone(), base.count)
+            sub.jump(jp)
+            sub.jump(jp)  # second call: cached table
+            torch.cuda.synchronize()
+            res[flag] = sub.states.cpu().numpy()
+        finally:
+            if old is None:
+                del os.environ["SLP_INIT_TABLES"]
+            else:
+                os.environ["SLP_INIT_TABLES"] = old
+    assert np.array_equal(res["1"], res["0"])
+    # spot check against the host jump
+    S0 = base.states.cpu().numpy().astype(np.uint64)
+    for i in (0, 12345, 69999):
+        g = P.Generator(spec, [int(v) for v in S0[:, i]], ptr=spec.kind.k - 1)
+        g.jump(jp)
+        g.jump(jp)
+        assert list(g.flat_words()) == [int(v) for v in res["1"][:, i].astype(np.uint64)]
