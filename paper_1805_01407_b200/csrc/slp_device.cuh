@@ -153,7 +153,7 @@ struct WOps<64> {
 #define SLP_ROT_POLICY 0  // 0: all rotations on the ALU; 1: Gen::best_mask (A/B: no gain, ptxas re-normalises)
 #endif
 #ifndef SLP_SUM_POLICY
-#define SLP_SUM_POLICY 0  // 0: IADD3 carry chains; 1: IMAD.WIDE accumulators
+#define SLP_SUM_POLICY 3  // 0: 128-bit carry chain per output; 1, 2: IMAD.WIDE accumulators; 3: half sums
 #endif
 
 // Pipe cost of one output, in warp instructions per 32 outputs
@@ -752,7 +752,10 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
 constexpr int kFusedThreads = 256;
 
 template <class G, bool MANT, bool F64>
-__global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
+#ifndef SLP_FUSED_MINB
+#define SLP_FUSED_MINB 1
+#endif
+__global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedParams p) {
   using word = typename G::word;
   constexpr int K = G::k;
   constexpr int CH = 16;  // multiple of every ring size
@@ -775,7 +778,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
   constexpr int MSK = G::best_mask(G::w == 64 ? 1 : 1, (G::w == 64 ? 2 : 1) + (MANT ? 1 : 0));
   const uint32_t one = p.one;
   uint64_t slo = 0, shi = 0, sx = 0, slow = 0;
-  double fs = 0.0;
+  double fs = 0.0, fs2 = 0.0;
   for (uint64_t u = (uint64_t)blockIdx.x * WPB + warp; u < p.nunits; u += (uint64_t)gridDim.x * WPB) {
     const uint64_t stream = u * 32 + lane;
     if (stream >= p.nstreams) continue;
@@ -817,6 +820,17 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
           lw = madlo((uint32_t)o0 & LOWMASK, one, lw);
           lw = madlo((uint32_t)o1 & LOWMASK, one, lw);
         }
+#elif SLP_SUM_POLICY == 3
+        // exact sum as two 64-bit sums of 32-bit halves, one output pair per
+        // 3-input add (IADD3 + IADD3.X per half): 2 ALU ops per output
+        // instead of a 128-bit carry chain per output (4)
+        if constexpr (MANT) {
+          acc_lo += (uint64_t)(uint32_t)o0 + (uint32_t)o1;
+          if constexpr (G::w == 64) acc_hi += ((uint64_t)o0 >> 32) + ((uint64_t)o1 >> 32);
+          lw += ((uint32_t)o0 & LOWMASK) + ((uint32_t)o1 & LOWMASK);
+        } else {
+          slo += (uint64_t)o0 + (uint64_t)o1;
+        }
 #else
         if constexpr (MANT) {
           add128(slo, shi, (uint64_t)o0);
@@ -827,13 +841,23 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
         }
 #endif
         xx ^= o0 ^ o1;
-        if constexpr (F64) {
+        if constexpr (F64) {  // two independent chains: the DADD latency, not the pipe, bounds one chain
           fs += __ull2double_rn((uint64_t)o0 >> SH);
-          fs += __ull2double_rn((uint64_t)o1 >> SH);
+          fs2 += __ull2double_rn((uint64_t)o1 >> SH);
         }
       }
       sx ^= (uint64_t)xx;
       slow += (uint64_t)lw + lw2;
+#if SLP_SUM_POLICY == 3
+      if constexpr (MANT) {
+        if ((c & ((1ull << 26) - 1)) == ((1ull << 26) - 1)) {  // every 2^30 outputs: keep the half sums < 2^64
+          add128(slo, shi, acc_lo);
+          add128(slo, shi, acc_hi << 32);
+          shi += acc_hi >> 32;
+          acc_lo = acc_hi = 0;
+        }
+      }
+#endif
     }
     for (uint64_t t = 0; t < rem; ++t) {
       const word x = G::next_flat(s);
@@ -855,6 +879,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedParams p) {
       for (int j = 0; j < K; ++j) sout[j * p.ld + stream] = s[j];
     }
   }
+  fs += fs2;
   // warp reduction (exact: 128-bit sums, xor; fixed shuffle order for fs)
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
