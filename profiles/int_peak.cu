@@ -27,6 +27,10 @@ __global__ void k(uint32_t *out, uint32_t seed) {
         asm volatile("shf.l.wrap.b32 %0, %0, %1, 13;" : "+r"(a[c]) : "r"(b[c]));
       } else if (OP == 2) {  // IMAD
         asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[c]) : "r"(b[c]), "r"(i));
+      } else if (OP == 4) {  // IMAD.WIDE (64-bit result)
+        uint64_t w;
+        asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(a[c]), "r"(b[c]), "l"((uint64_t)i));
+        a[c] = (uint32_t)w ^ (uint32_t)(w >> 32);
       } else {  // ALU + FMA interleaved
         if (c & 1)
           asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[c]) : "r"(b[c]), "r"(i));
@@ -50,7 +54,7 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const char *names[] = {"LOP3 (ALU)", "SHF.L.W (ALU)", "IMAD (FMA)", "LOP3+IMAD mix"};
+  const char *names[] = {"LOP3 (ALU)", "SHF.L.W (ALU)", "IMAD (FMA)", "LOP3+IMAD mix", "IMAD.WIDE (+1 LOP3 fold)"};
   auto run = [&](int op, auto kern) {
     const int grid = sms * 8, block = 256;
     kern<<<grid, block>>>(out, 1);
@@ -74,5 +78,6 @@ int main() {
   run(1, k<1>);
   run(2, k<2>);
   run(3, k<3>);
+  run(4, k<4>);
   return 0;
 }
