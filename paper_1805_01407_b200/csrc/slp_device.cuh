@@ -59,12 +59,17 @@ __device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {
 
 // Word operations.  64-bit words are manipulated as explicit 32-bit halves.
 // The generators are integer-issue bound on the ALU pipe (LOP3/SHF/IADD3,
-// profiles/), so every rotation has two forms:
-//   rotl   : two funnel shifts (SHF.L.W)                 -> 2 ALU
-//   rotl_f : three wide multiply-adds by 2^r             -> 3 FMA
-// and the kernels pick, per generator, the mix that balances the two pipes
-// (Gen::best_mask).  Constant left shifts are 2 FMA (IMAD.WIDE + IMAD),
-// multiplication by a constant < 2^32 is 2 FMA (3 for a 64-bit constant).
+// profiles/).  Measured on sm_100 (profiles/int_peak.cu): LOP3, SHF and IMAD
+// issue at 2 per SM per cycle, IMAD.HI at 1, IMAD.WIDE at 0.5.  Hence:
+//   rotl   : two funnel shifts (SHF.L.W)                 -> 2 ALU  (default)
+//   rotl_f : three wide multiply-adds by 2^r             -> 3 FMA  (A/B only:
+//            Gen::best_mask with SLP_ROT_POLICY=1 loses to IMAD.WIDE's rate)
+//   shl    : IMAD.SHL (low half) + SHF.L.U64.HI          -> 1 FMA + 1 ALU
+//   mulc   : IMAD.WIDE + IMAD (+ IMAD for a 64-bit constant).
+#ifndef SLP_MUL_POLICY
+#define SLP_MUL_POLICY 1  // 0: shifts via IMAD.WIDE; 1: 64-bit constant shifts as IMAD.SHL + SHF; 2: also x*(2^a+1) as LEA pairs
+#endif
+
 template <int W>
 struct WOps;
 
@@ -129,9 +134,15 @@ struct WOps<64> {
   }
   template <int B>
   static __device__ __forceinline__ word shl(word x) {
+#if SLP_MUL_POLICY >= 1
+    // IMAD.SHL (lo) + SHF.L.U64.HI (hi): IMAD.WIDE issues at a quarter of the
+    // IMAD rate on sm_100 (profiles/int_peak.cu)
+    return x << B;
+#else
     if constexpr (B >= 32) return pack(0u, lo(x) << (B - 32));
     const uint64_t w = mulw(lo(x), 1u << B);
     return pack((uint32_t)w, madlo(hi(x), 1u << B, (uint32_t)(w >> 32)));
+#endif
   }
   template <int B>
   static __device__ __forceinline__ word shr(word x) {
@@ -140,6 +151,12 @@ struct WOps<64> {
   }
   template <unsigned long long C>
   static __device__ __forceinline__ word mulc(word x) {
+#if SLP_MUL_POLICY == 2
+    // 2^a + 1 (the ** constants 5 and 9): x + (x << a) = LEA + LEA.HI.X, which
+    // issue at up to twice the single-pipe rate, instead of IMAD.WIDE + IMAD
+    constexpr int a = (C > 1 && ((C - 1) & (C - 2)) == 0) ? __builtin_ctzll(C - 1) : -1;
+    if constexpr (a > 0 && a < 32) return x + (x << a);
+#endif
     const uint64_t p = mulw(lo(x), (uint32_t)C);
     uint32_t h = madlo(hi(x), (uint32_t)C, (uint32_t)(p >> 32));
     if constexpr ((C >> 32) != 0) h = madlo(lo(x), (uint32_t)(C >> 32), h);

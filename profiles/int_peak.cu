@@ -31,6 +31,10 @@ __global__ void k(uint32_t *out, uint32_t seed) {
         uint64_t w;
         asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(a[c]), "r"(b[c]), "l"((uint64_t)i));
         a[c] = (uint32_t)w ^ (uint32_t)(w >> 32);
+      } else if (OP == 5) {  // IMAD.HI
+        asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(a[c]) : "r"(b[c]));
+      } else if (OP == 6) {  // LEA-style 64-bit x*5 = x + (x << 2) via add.cc (lo) / addc (hi)
+        asm volatile("{\n\t.reg .u32 t;\n\tshl.b32 t, %0, 2;\n\tadd.u32 %0, %0, t;\n\t}" : "+r"(a[c]));
       } else {  // ALU + FMA interleaved
         if (c & 1)
           asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[c]) : "r"(b[c]), "r"(i));
@@ -54,7 +58,8 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const char *names[] = {"LOP3 (ALU)", "SHF.L.W (ALU)", "IMAD (FMA)", "LOP3+IMAD mix", "IMAD.WIDE (+1 LOP3 fold)"};
+  const char *names[] = {"LOP3 (ALU)", "SHF.L.W (ALU)", "IMAD (FMA)", "LOP3+IMAD mix", "IMAD.WIDE (+1 LOP3 fold)",
+                         "IMAD.HI", "x + (x << 2) (LEA)"};
   auto run = [&](int op, auto kern) {
     const int grid = sms * 8, block = 256;
     kern<<<grid, block>>>(out, 1);
@@ -79,5 +84,7 @@ int main() {
   run(2, k<2>);
   run(3, k<3>);
   run(4, k<4>);
+  run(5, k<5>);
+  run(6, k<6>);
   return 0;
 }
