@@ -269,7 +269,7 @@ def run_ours(args):
             e2e = {"error": pin_err or "pinned allocation failed on another rank"}
             host = None
     if host is not None:
-        bufs = [torch.empty((1 << 17, T), dtype=torch.uint64, device=dev) for _ in range(2)]
+        bufs = [torch.empty((1 << 15, T), dtype=torch.uint64, device=dev) for _ in range(2)]
         del out
         for i in range(args.e2e_steps + 1):
             if i == 1:

@@ -291,7 +291,7 @@ def fused_checksum(spec: GeneratorSpec, states: torch.Tensor, T: int, *, exact: 
 
 
 def fill_to_host(spec: GeneratorSpec, states: torch.Tensor, T: int, host_out: torch.Tensor, *,
-                 kind: str = "native", slice_streams: int = 1 << 17, _bufs: list | None = None) -> torch.Tensor:
+                 kind: str = "native", slice_streams: int = 1 << 15, _bufs: list | None = None) -> torch.Tensor:
     """Stream-major fill delivered to HOST memory: the GPU generates slices of
     ``slice_streams`` substreams into two device buffers while a copy stream
     moves the previous slice to ``host_out`` (pinned (n, T) tensor), so the
