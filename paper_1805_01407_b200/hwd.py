@@ -315,18 +315,38 @@ class _GpuCounter:
 def _global_totals(counter, group):
     """Counters summed over all ranks (one all-reduce of the 2 x 3^k totals;
     a plain copy on one rank), as numpy uint64 arrays."""
+    return _totals_async(counter, group)()
+
+
+def _totals_async(counter, group):
+    """Enqueue a snapshot of the (all-reduced) counters and return a function
+    that waits for it.  On the GPU the snapshot is a device copy, the
+    all-reduce and an async copy to pinned memory, all ordered on the
+    current stream, so counting of the next range can be enqueued before
+    the host waits for this one."""
     import torch
 
     cnt, ws = counter.totals()
-    both = torch.cat([cnt, ws])
+    both = torch.cat([cnt, ws])  # a copy: later ranges keep counting into cnt / ws
     if group is not None:
         import torch.distributed as dist
 
-        both = both.clone()
         dist.all_reduce(both, op=dist.ReduceOp.SUM, group=group)
-    both = both.cpu().numpy().view(np.uint64)
     n = cnt.numel()
-    return both[:n], both[n:]
+    if not both.is_cuda:
+        host = both.numpy().view(np.uint64)
+        return lambda: (host[:n], host[n:])
+    host = torch.empty(both.shape, dtype=both.dtype, pin_memory=True)
+    host.copy_(both, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+
+    def wait():
+        ev.synchronize()
+        h = host.numpy().view(np.uint64)
+        return h[:n], h[n:]
+
+    return wait
 
 
 def run_generator(spec_or_name, config: HwdConfig, seed: int = 1, checkpoint_start: int | None = None,
@@ -381,6 +401,26 @@ def run_generator(spec_or_name, config: HwdConfig, seed: int = 1, checkpoint_sta
                          faulty_category=ck.faulty_category if ck else 0, w=config.w, k=config.k,
                          ell=config.ell, mode=config.mode, overflow=False, history=history)
 
+    # The checkpoint schedule is fixed in advance (doubling targets, the byte
+    # limit, the end of the source); only a failing checkpoint stops early.
+    # Counting of range i+1 is enqueued before checkpoint i is evaluated on
+    # the host, so evaluations overlap the GPU (a stop discards the extra range).
+    pending = []  # (seen, at_cp, at_limit, wait)
+
+    def evaluate(item):
+        at_seen, at_cp, at_limit, wait = item
+        cnt, ws = wait()
+        ck = evaluate_counts(cnt, ws, config, at_seen)
+        history.append(ck)
+        nonlocal seen
+        if ck.p_value < config.p_threshold:
+            seen = at_seen
+            return report("failed", ck)
+        if at_limit:
+            seen = at_seen
+            return report("passed", ck)
+        return None
+
     while seen < stream_end:
         target = min(next_cp, value_limit, stream_end)
         lo_pos = max(seen, config.k)
@@ -388,16 +428,20 @@ def run_generator(spec_or_name, config: HwdConfig, seed: int = 1, checkpoint_sta
             count_range(lo_pos, target)
         seen = target
         at_cp, at_limit = seen >= next_cp, seen >= value_limit
+        if at_cp:
+            next_cp *= 2
         if at_cp or at_limit:
-            cnt, ws = _global_totals(counter, group)
-            ck = evaluate_counts(cnt, ws, config, seen)
-            history.append(ck)
-            if at_cp:
-                next_cp *= 2
-            if ck.p_value < config.p_threshold:
-                return report("failed", ck)
-            if at_limit:
-                return report("passed", ck)
+            pending.append((seen, at_cp, at_limit, _totals_async(counter, group)))
+        while len(pending) > (0 if at_limit else 1):
+            r = evaluate(pending.pop(0))
+            if r is not None:
+                return r
+        if at_limit:
+            break
+    while pending:
+        r = evaluate(pending.pop(0))
+        if r is not None:
+            return r
     ck = None
     if seen > config.k:
         cnt, ws = _global_totals(counter, group)
