@@ -416,11 +416,17 @@ __device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t x) {
 //                With B buffers per warp, store i-B must have finished reading
 //                before tile i overwrites its buffer (cp.async.bulk.wait_group.read).
 //   FILL_STAGED  stream-major, same staging, element stores (any pitch/alignment);
-//   FILL_POS     position-major: each output is one coalesced warp store.
+//   FILL_POS     position-major: each output is one coalesced warp store
+//                (any pitch/alignment);
+//   FILL_POS_TMA position-major through the same per-warp tile, laid out
+//                [position][lane]: one 2-D TMA store writes CH rows of the
+//                output x 32 consecutive substreams (256 B for u64).  Direct
+//                stores leave 256-byte pieces scattered over CH rows that
+//                are 8 MiB apart and ran at 2.5-5.5 TB/s.
 // Shared-memory tile layout [seg][row][128 B], chunk q of (seg, row) at
 // ((seg*32 + row) * 128) + ((q ^ (row & 7)) << 4)  (CU_TENSOR_MAP_SWIZZLE_128B).
 
-enum { FILL_TMA = 0, FILL_STAGED = 1, FILL_POS = 2 };
+enum { FILL_TMA = 0, FILL_STAGED = 1, FILL_POS = 2, FILL_POS_TMA = 3 };
 constexpr int kFillThreads = kFillWarps * 32;
 
 // Fill tile configurations (slp_ops.h):
@@ -595,7 +601,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       const uint64_t pos0 = c * CH;
       uint32_t tile = 0;
       auto wait_buffer = [&] {
-        if constexpr (MODE == FILL_TMA) {
+        if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA) {
           if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
         }
         __syncwarp();
@@ -603,6 +609,18 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       // one 16-byte chunk (outputs b+e .. b+e+EPC-1 of this lane's row) into the
       // tile; b (runtime) is a sub-block start, e (compile time) the offset in it
       auto put = [&](uint32_t b, int e, const bits(&v)[EPC]) {
+        if constexpr (MODE == FILL_POS_TMA) {  // tile [position][lane]
+          const uint32_t row = tile + (b * 32 + lane) * ES;
+#pragma unroll
+          for (int i = 0; i < EPC; ++i) {
+            const uint32_t addr = row + (e + i) * 32 * ES;
+            if constexpr (ES == 8)
+              asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"((uint64_t)v[i]) : "memory");
+            else
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"((uint32_t)v[i]) : "memory");
+          }
+          return;
+        }
         const int byte = e * ES;
         const uint32_t addr = tile + ((b * ES / 128) << 12) + swz(byte >> 7, lane, (byte & 127) >> 4);
         if constexpr (ES == 8) {
@@ -707,6 +725,14 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
           bulk_commit();
         }
         ++issued;
+      } else if constexpr (MODE == FILL_POS_TMA) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (elect_one()) {
+          tma_store_2d(&tmap, tile, (int)row0, (int)pos0);
+          bulk_commit();
+        }
+        ++issued;
       } else if constexpr (MODE == FILL_STAGED) {
         __syncwarp();
         // element stores; CPR lanes cover one 128-byte segment of a row
@@ -741,7 +767,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       }
       if (valid) {
         const uint64_t pos = ntiles * CH + t;
-        if constexpr (MODE == FILL_POS)
+        if constexpr (MODE == FILL_POS || MODE == FILL_POS_TMA)
           out[pos * p.ld_out + stream] = x;
         else
           out[stream * p.ld_out + pos] = x;
@@ -752,7 +778,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       for (int j = 0; j < K; ++j) sout[j * p.ld + stream] = s[j];
     }
   }
-  if constexpr (MODE == FILL_TMA) {
+  if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA) {
     if (elect_one()) bulk_wait_all<0>();
   }
   if constexpr (CSUM) reduce_checksum_block<kFillWarps>(cs_lo, cs_hi, cs_x, cs_low, 0.0, p.partials);
@@ -1125,6 +1151,10 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
   if constexpr (MODE == FILL_TMA) {
     int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, FillShape<G, fill_kind<OK, CSUM>()>::segs);
     if (rc != SLP_OK) return rc;
+  } else if constexpr (MODE == FILL_POS_TMA) {
+    int rc = make_store_tmap_pm(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out,
+                                FillShape<G, fill_kind<OK, CSUM>()>::row_bytes / ES);
+    if (rc != SLP_OK) return rc;
   }
   auto kern = k_fill<G, OK, MODE, CSUM>;
   const int smem = MODE == FILL_POS ? 0 : FillShape<G, fill_kind<OK, CSUM>()>::smem;
@@ -1195,7 +1225,10 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
   const int es = (ok == SLP_OUT_NATIVE) ? W / 8 : (ok == SLP_OUT_F32 ? 4 : 8);
   int mode;
   if (layout == SLP_POSITION_MAJOR)
-    mode = FILL_POS;
+    mode = tma_ok_pm(p.out, es, p.T, p.nstreams, p.ld_out,
+                     fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs * 128 / es)
+               ? FILL_POS_TMA
+               : FILL_POS;
   else if (layout == SLP_STREAM_MAJOR)
     mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out,
                   fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs)
@@ -1207,6 +1240,7 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
   if (ok == OKV) {                                                             \
     if (mode == FILL_TMA) return launch_fill<G, OKV, FILL_TMA>(p, st);         \
     if (mode == FILL_STAGED) return launch_fill<G, OKV, FILL_STAGED>(p, st);   \
+    if (mode == FILL_POS_TMA) return launch_fill<G, OKV, FILL_POS_TMA>(p, st); \
     return launch_fill<G, OKV, FILL_POS>(p, st);                               \
   }
   if constexpr (W == 64) {

@@ -57,6 +57,10 @@ def test_all_kinds_vs_oracle(name, T):
         got = sub.fill(T, kind=kind).cpu().numpy()
         np.testing.assert_array_equal(_bits(got), _bits(exp), err_msg=f"{name} {kind}")
         np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
+        # position-major (2-D TMA path for T >= one tile) is the transpose
+        sub = D.Substreams.from_states(spec, flat)
+        gotp = sub.fill(T, kind=kind, layout="position").cpu().numpy()
+        np.testing.assert_array_equal(_bits(gotp), _bits(exp.T.copy()), err_msg=f"{name} {kind} position")
         if kind in ("native", "f64", "f32"):
             sub = D.Substreams.from_states(spec, flat)
             out, c = D.fill_checksum(spec, sub.states, T, kind=kind)
@@ -79,6 +83,8 @@ def test_many_units_per_warp(name):
     got = sub.fill(T).cpu().numpy()
     np.testing.assert_array_equal(got, want)
     np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
+    sub = D.Substreams.from_states(spec, flat)
+    np.testing.assert_array_equal(sub.fill(T, layout="position").cpu().numpy(), want.T)
     sub = D.Substreams.from_states(spec, flat)
     _, c = D.fill_checksum(spec, sub.states, T)
     oc = O.checksum(want, w)
