@@ -143,6 +143,17 @@ int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, co
 int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams,
              uint64_t T, int out_kind, int layout, void *out, uint64_t ld_out, void *stream);
 
+/* One superbatch of the reference's laned single stream (LanedStream,
+ * generators.py:426-490): lane j = base * M^(j * lane_len) is set
+ * up in `states` (device SoA (k, lanes), ld = lanes), then lane_len outputs
+ * of every lane are written stream-major to out[lanes][lane_len] -- i.e. the
+ * next lanes*lane_len values of the scalar stream of `base_flat`, in order.
+ * `states` is left advanced by lane_len; the next superbatch is
+ * slp_jump_states by (lanes - 1) * lane_len, then slp_fill (:487-490).
+ * out_kind: NATIVE, U64 (the reference's uint64 chunks for w = 32), F64/F32. */
+int slp_laned_fill(int id, const uint64_t *base_flat, uint64_t lanes, uint64_t lane_len, int out_kind,
+                   void *out, void *states, void *stream);
+
 /* Store AND reduce in one pass: slp_fill (stream-major, TMA-eligible output)
  * that also writes the exact checksum of the integer outputs (as slp_fused
  * with SLP_FUSE_EXACT) to `result` (device).  BASELINE config 3 "store mode

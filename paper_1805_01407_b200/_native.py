@@ -80,6 +80,8 @@ SIGNATURES = {
                                             ctypes.c_uint64, vp, ctypes.c_uint64, vp]),
     "slp_fill": (ctypes.c_int, [ctypes.c_int, vp, vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                 ctypes.c_int, ctypes.c_int, vp, ctypes.c_uint64, vp]),
+    "slp_laned_fill": (ctypes.c_int, [ctypes.c_int, u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, vp, vp,
+                                      vp]),
     "slp_fill_checksum": (ctypes.c_int, [ctypes.c_int, vp, vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_int, vp, ctypes.c_uint64, vp, vp, ctypes.c_size_t, vp]),
     "slp_fused_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_uint64]),

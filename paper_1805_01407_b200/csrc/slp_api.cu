@@ -567,6 +567,17 @@ int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *sr
   return ops->jump(p, &base, true, 1, st);
 }
 
+int slp_laned_fill(int id, const uint64_t *base_flat, uint64_t lanes, uint64_t lane_len, int out_kind, void *out,
+                   void *states, void *stream) {
+  if (!gen_desc(id)) return SLP_ERR_UNKNOWN_GENERATOR;
+  if (lanes == 0 || lane_len == 0) return SLP_OK;
+  if (!base_flat || !out || !states) return SLP_ERR_INVALID;
+  const uint64_t steps[1] = {lane_len};
+  int rc = slp_init_substreams(id, base_flat, 1, steps, 1, states, lanes, lanes, stream);
+  if (rc != SLP_OK) return rc;
+  return slp_fill(id, states, states, lanes, lanes, lane_len, out_kind, SLP_STREAM_MAJOR, out, lane_len, stream);
+}
+
 int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams, uint64_t T,
              int out_kind, int layout, void *out, uint64_t ld_out, void *stream) {
   const GenDesc *g = gen_desc(id);

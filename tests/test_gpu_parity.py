@@ -379,3 +379,33 @@ def test_host_chunks_are_fresh_and_match_device_chunks():
             assert not np.shares_memory(host[a], host[b])
     host[0][:] = 0  # caller owns it: later chunks are unaffected
     assert np.array_equal(host[1], dev[1])
+
+
+@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro1024plusplus", "xoshiro128plusplus"])
+def test_laned_fill_c_abi_superbatch(name):
+    """slp_laned_fill (C ABI) = the first lanes*lane_len values of
+    the scalar stream; then slp_jump_states + slp_fill give the next superbatch."""
+    import ctypes
+
+    from paper_1805_01407_b200 import _native
+
+    spec = P.get_spec(name)
+    lanes, lane_len = 96, 300
+    want = O.laned_stream(name, 42, 2 * lanes * lane_len, lanes, lane_len)
+    L = _native.lib()
+    gid = L.slp_generator_id(name.encode())
+    base = (ctypes.c_uint64 * spec.kind.k)(*O.seed_flat(name, 42))
+    states = torch.empty((spec.kind.k, lanes), dtype=torch.uint64 if spec.kind.w == 64 else torch.uint32,
+                         device="cuda")
+    out = torch.empty((lanes, lane_len), dtype=torch.uint64, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert L.slp_laned_fill(gid, base, lanes, lane_len, _native.OUT_U64, ctypes.c_void_p(out.data_ptr()),
+                            ctypes.c_void_p(states.data_ptr()), st) == 0
+    np.testing.assert_array_equal(out.cpu().numpy().reshape(-1), want[: lanes * lane_len])
+    jp = P.compute_jump_poly(spec, (lanes - 1) * lane_len)
+    pw, pn = _native.int_to_words(jp.poly.bits)
+    sp = ctypes.c_void_p(states.data_ptr())
+    assert L.slp_jump_states(gid, pw, pn, sp, lanes, sp, lanes, lanes, st) == 0
+    assert L.slp_fill(gid, sp, sp, lanes, lanes, lane_len, _native.OUT_U64, _native.STREAM_MAJOR,
+                      ctypes.c_void_p(out.data_ptr()), lane_len, st) == 0
+    np.testing.assert_array_equal(out.cpu().numpy().reshape(-1), want[lanes * lane_len:])
