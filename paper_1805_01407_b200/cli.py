@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 
 from . import generators
@@ -72,6 +73,26 @@ _RAW_LANE_LEN = 1024
 _RAW_MAX_LANES = 1 << 16
 
 
+def _grow_pipe(out) -> None:
+    """A 64 KiB pipe caps the raw stream at ~3 GB/s; ask for the largest
+    pipe the system allows (Linux F_SETPIPE_SZ, /proc/sys/fs/pipe-max-size)."""
+    try:
+        import fcntl
+        import stat
+
+        fd = out.fileno()
+        if not stat.S_ISFIFO(os.fstat(fd).st_mode):
+            return
+        try:
+            with open("/proc/sys/fs/pipe-max-size") as f:
+                size = int(f.read())
+        except OSError:
+            size = 1 << 20
+        fcntl.fcntl(fd, fcntl.F_SETPIPE_SZ, size)
+    except (OSError, AttributeError, ValueError, ImportError):
+        pass
+
+
 def write_raw(spec: GeneratorSpec, gen: Generator, n: int, out) -> None:
     """Little-endian w-bit words of the stream of ``gen`` (n values) to ``out``."""
     import numpy as np
@@ -81,6 +102,7 @@ def write_raw(spec: GeneratorSpec, gen: Generator, n: int, out) -> None:
     lanes = max(1, min(_RAW_MAX_LANES, -(-n // _RAW_LANE_LEN)))
     stream = generators.LanedStream(spec, generator=gen, lanes=lanes, lane_len=_RAW_LANE_LEN)
     dtype = np.dtype("<u8") if spec.kind.w == 64 else np.dtype("<u4")
+    _grow_pipe(out)
     # pipelined GPU -> pinned staging -> output, no intermediate copies
     for chunk in stream.chunks(n, native=True, _views=True):
         out.write(memoryview(chunk.astype(dtype, copy=False)).cast("B"))
