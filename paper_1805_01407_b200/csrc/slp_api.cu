@@ -704,7 +704,23 @@ int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, ui
   for (int j = 1; j < k; ++j) pw *= 3;
   p.pow3k1 = pw;
   p.ncells = pw * 3;
-  p.global_cells = k > 9 ? 1 : 0;
+  // k <= 9: all 3^k packed cells in one CTA's shared memory (<= 77 KB).
+  // k = 10, 11: slices of <= 24K cells (96 KB, two CTAs per SM), each CTA
+  // regenerating its segments per slice (measured 1.5e11 / 5.1e10 values/s
+  // against 6.2e10 / ~4e10 with global atomics).  Beyond kMaxHwdSlices slices
+  // (k >= 12) the repeated generation costs more than 64-bit global atomics.
+  // SLP_HWD_SLICES=0 forces global atomics for k > 9 (A/B, tests).
+  constexpr uint32_t kSliceCells = 24576, kMaxHwdSlices = 8;
+  const char *ev = std::getenv("SLP_HWD_SLICES");
+  const bool allow_slices = !(ev && *ev == '0');
+  if (p.ncells <= 19683) {
+    p.global_cells = 0;
+    p.slice_cells = p.ncells;
+  } else {
+    const uint32_t nsl = (p.ncells + kSliceCells - 1) / kSliceCells;
+    p.global_cells = (allow_slices && nsl <= kMaxHwdSlices) ? 0 : 1;
+    p.slice_cells = (p.ncells + nsl - 1) / nsl;
+  }
   p.g_counts = reinterpret_cast<unsigned long long *>(counts);
   p.g_sums = reinterpret_cast<unsigned long long *>(sums);
   p.overflow_ctas = reinterpret_cast<unsigned long long *>(overflow_ctas);

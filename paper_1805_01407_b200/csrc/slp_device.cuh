@@ -1380,9 +1380,13 @@ int jump_table_impl(const TableJumpParams &p, uint64_t nbatch, cudaStream_t st) 
 constexpr int kHwdThreads = 256;
 constexpr uint32_t kHwdRecip = 0x55555556u;  // ceil(2^32 / 3), hwd.py:44
 
-// counts one thread's segment; GLOBAL: 64-bit global atomics, else packed smem cells
-template <class G, bool TRANS, bool SPLIT, bool GLOBAL>
-__device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, uint32_t *cells) {
+// counts one thread's segment; GLOBAL: 64-bit global atomics, else packed smem
+// cells.  SLICED: only signatures in [cell_lo, cell_lo + p.slice_cells) are
+// counted (3^k cells split over the CTAs of blockIdx.y); returns the number
+// of values counted.
+template <class G, bool TRANS, bool SPLIT, bool GLOBAL, bool SLICED = false>
+__device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, uint32_t *cells,
+                                                uint32_t cell_lo = 0) {
   using word = typename G::word;
   constexpr int K = G::k;
   constexpr int TW = SPLIT ? 32 : G::w;  // test-value width
@@ -1392,7 +1396,7 @@ __device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, 
   for (int j = 0; j < K; ++j) s[j] = sin[j * p.ld + i];
   // cnt <= tseg < 2^16 and warm <= k + 2: 32-bit counters
   uint32_t cnt = (uint32_t)((i + 1) * p.tseg <= p.total ? p.tseg : p.total - i * p.tseg);
-  const uint32_t counted = cnt;
+  uint32_t counted = SLICED ? 0u : cnt;
   uint32_t warm = (uint32_t)(i == 0 ? p.warm0 : p.warm);
   uint32_t sig = 0;
   uint64_t prev = 0;
@@ -1407,7 +1411,18 @@ __device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, 
     const int nu = TW == 64 ? __popcll(x) : __popc((uint32_t)x);
     const uint32_t t = (uint32_t)(nu >= lo) + (uint32_t)(nu > hi);
     if (count) {
-      if constexpr (GLOBAL) {
+      if constexpr (SLICED) {
+        const uint32_t rel = sig - cell_lo;
+        if (rel < p.slice_cells) {
+          ++counted;
+          if constexpr (GLOBAL) {
+            atomicAdd(p.g_counts + sig, 1ull);
+            atomicAdd(p.g_sums + sig, (unsigned long long)nu);
+          } else {
+            atomicAdd(cells + rel, (1u << 19) | (uint32_t)nu);
+          }
+        }
+      } else if constexpr (GLOBAL) {
         atomicAdd(p.g_counts + sig, 1ull);
         atomicAdd(p.g_sums + sig, (unsigned long long)nu);
       } else {
@@ -1473,65 +1488,80 @@ __device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, 
   return counted;
 }
 
-template <class G, bool TRANS, bool SPLIT>
+// SLICED (k >= 10): 3^k packed cells exceed shared memory, so the cells are
+// split into gridDim.y slices; CTA (x, y) regenerates the segments of CTA
+// column x and counts only the signatures of slice y.  Generation is repeated
+// per slice, but every count stays a shared-memory atomic (global 64-bit
+// atomics are 8-20x slower per value).
+template <class G, bool TRANS, bool SPLIT, bool SLICED>
 __global__ void __launch_bounds__(kHwdThreads) k_hwd(HwdParams p) {
   extern __shared__ uint32_t cells[];
   __shared__ unsigned long long s_counted, s_cellsum;
   const int tid = threadIdx.x;
   const uint64_t i = (uint64_t)blockIdx.x * kHwdThreads + tid;
-  if (p.global_cells) {  // 3^k cells do not fit in shared memory (k > 9)
+  if (p.global_cells) {  // 3^k cells do not fit in shared memory even when sliced
     if (i < p.nthreads) hwd_segment<G, TRANS, SPLIT, true>(p, i, nullptr);
     return;
   }
-  for (uint32_t c = tid; c < p.ncells; c += kHwdThreads) cells[c] = 0u;
+  const uint32_t cell_lo = SLICED ? blockIdx.y * p.slice_cells : 0u;
+  const uint32_t nc = SLICED ? (p.ncells - cell_lo < p.slice_cells ? p.ncells - cell_lo : p.slice_cells) : p.ncells;
+  for (uint32_t c = tid; c < nc; c += kHwdThreads) cells[c] = 0u;
   if (tid == 0) s_counted = s_cellsum = 0ull;
   __syncthreads();
   uint32_t mine = 0;
-  if (i < p.nthreads) mine = hwd_segment<G, TRANS, SPLIT, false>(p, i, cells);
+  if (i < p.nthreads) mine = hwd_segment<G, TRANS, SPLIT, false, SLICED>(p, i, cells, cell_lo);
   atomicAdd(&s_counted, (unsigned long long)mine);
   __syncthreads();
   unsigned long long part = 0;
-  for (uint32_t c = tid; c < p.ncells; c += kHwdThreads) part += cells[c] >> 19;
+  for (uint32_t c = tid; c < nc; c += kHwdThreads) part += cells[c] >> 19;
   atomicAdd(&s_cellsum, part);
   __syncthreads();
   if (s_cellsum == s_counted) {  // conservation holds: no packed cell overflowed
-    for (uint32_t c = tid; c < p.ncells; c += kHwdThreads) {
+    for (uint32_t c = tid; c < nc; c += kHwdThreads) {
       const uint32_t cell = cells[c];
       if (cell) {
-        atomicAdd(p.g_counts + c, (unsigned long long)(cell >> 19));
-        atomicAdd(p.g_sums + c, (unsigned long long)(cell & 0x7FFFFu));
+        atomicAdd(p.g_counts + cell_lo + c, (unsigned long long)(cell >> 19));
+        atomicAdd(p.g_sums + cell_lo + c, (unsigned long long)(cell & 0x7FFFFu));
       }
     }
-  } else {  // recount this CTA's segments exactly (rare: heavily skewed streams)
+  } else {  // recount this CTA's segments (its slice) exactly (rare: heavily skewed streams)
     if (tid == 0 && p.overflow_ctas) atomicAdd(p.overflow_ctas, 1ull);
-    if (i < p.nthreads) hwd_segment<G, TRANS, SPLIT, true>(p, i, nullptr);
+    if (i < p.nthreads) hwd_segment<G, TRANS, SPLIT, true, SLICED>(p, i, nullptr, cell_lo);
   }
 }
 
-template <class G, bool TRANS, bool SPLIT>
+template <class G, bool TRANS, bool SPLIT, bool SLICED>
 int launch_hwd_t(const HwdParams &p, cudaStream_t st) {
-  auto kern = k_hwd<G, TRANS, SPLIT>;
-  const size_t smem = p.global_cells ? 0 : (size_t)p.ncells * sizeof(uint32_t);
+  auto kern = k_hwd<G, TRANS, SPLIT, SLICED>;
+  const uint32_t cells = SLICED ? p.slice_cells : p.ncells;
+  const size_t smem = p.global_cells ? 0 : (size_t)cells * sizeof(uint32_t);
   if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
                               cudaSuccess)
     return cuda_fail("cudaFuncSetAttribute(hwd)");
   const uint64_t grid = (p.nthreads + kHwdThreads - 1) / kHwdThreads;
   if (grid == 0) return SLP_OK;
-  if (grid > 0x7fffffffull) return SLP_ERR_INVALID;
-  kern<<<(unsigned)grid, kHwdThreads, smem, st>>>(p);
+  const uint64_t slices = SLICED ? (p.ncells + p.slice_cells - 1) / p.slice_cells : 1;
+  if (grid > 0x7fffffffull || slices > 65535) return SLP_ERR_INVALID;
+  kern<<<dim3((unsigned)grid, (unsigned)slices), kHwdThreads, smem, st>>>(p);
   return check_launch("k_hwd");
 }
 
 template <class G>
 int hwd_impl(const HwdParams &p, int transitional, int split, cudaStream_t st) {
+  const bool sliced = !p.global_cells && p.slice_cells < p.ncells;
+#define SLP_HWD_LAUNCH(TR, SP)                                                              \
+  return sliced ? launch_hwd_t<G, TR, SP, true>(p, st) : launch_hwd_t<G, TR, SP, false>(p, st)
   if (split) {
     if constexpr (G::w == 64) {
-      return transitional ? launch_hwd_t<G, true, true>(p, st) : launch_hwd_t<G, false, true>(p, st);
+      if (transitional) SLP_HWD_LAUNCH(true, true);
+      SLP_HWD_LAUNCH(false, true);
     } else {
       return SLP_ERR_INVALID;  // split needs 64-bit source words
     }
   }
-  return transitional ? launch_hwd_t<G, true, false>(p, st) : launch_hwd_t<G, false, false>(p, st);
+  if (transitional) SLP_HWD_LAUNCH(true, false);
+  SLP_HWD_LAUNCH(false, false);
+#undef SLP_HWD_LAUNCH
 }
 
 template <class G>

@@ -93,7 +93,9 @@ struct HwdParams {
   int lo, hi;                // trit thresholds: nu < lo -> 0, nu <= hi -> 1, else 2
   uint32_t pow3k1;           // 3^(k-1)
   uint32_t ncells;           // 3^k
-  int global_cells;          // 1: count straight into global memory (k > 9)
+  int global_cells;          // 1: count straight into global memory (3^k too large even when sliced)
+  uint32_t slice_cells;      // shared-memory cells per CTA; CTA (x, y) counts signatures in
+                             // [y * slice_cells, (y + 1) * slice_cells) (gridDim.y slices)
   unsigned long long *g_counts, *g_sums;  // 3^k each, accumulated
   unsigned long long *overflow_ctas;      // nullable: CTAs that fell back to the exact recount
 };

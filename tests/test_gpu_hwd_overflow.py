@@ -29,3 +29,39 @@ def test_overflowing_ctas_recount_exactly(mode, split):
     np.testing.assert_array_equal(a_cnt, b_cnt)
     np.testing.assert_array_equal(a_sum, b_sum)
     assert int(a_cnt.sum()) == c1 - c0
+
+
+@pytest.mark.parametrize("k,mode,split", [(10, "standard", False), (11, "transitional", False),
+                                          (10, "standard", True), (12, "standard", False)])  # k=12: global path
+def test_sliced_cells_equal_global_atomics_and_oracle(k, mode, split):
+    """k >= 10: 3^k cells split over CTA slices in shared memory (each slice
+    regenerates its segments) give exactly the counts of 64-bit global atomics
+    (SLP_HWD_SLICES=0) and of the CPU oracle."""
+    import os
+
+    from oracle import oracle as O
+
+    w = 32 if split else 64
+    cfg = hwd.HwdConfig(w=w, k=k, mode=mode, split=split)
+    spec = hwd.get_spec("xoroshiro128plus")
+    c0, c1 = k, 300_000
+    res = {}
+    for flag in ("1", "0"):
+        old = os.environ.get("SLP_HWD_SLICES")
+        os.environ["SLP_HWD_SLICES"] = flag
+        try:
+            ctr = hwd._GpuCounter(spec, 3, cfg)
+            ctr.count(c0, c1)
+            res[flag] = ctr.snapshot()
+        finally:
+            if old is None:
+                del os.environ["SLP_HWD_SLICES"]
+            else:
+                os.environ["SLP_HWD_SLICES"] = old
+    np.testing.assert_array_equal(res["1"][0], res["0"][0])
+    np.testing.assert_array_equal(res["1"][1], res["0"][1])
+    assert int(res["1"][0].sum()) == c1 - c0
+    vals = O.hwd_test_values("xoroshiro128plus", 3, c1, split, mode == "transitional", w)
+    want_c, want_s = O.hwd_counts(vals, c0, c1, k, w, cfg.ell)
+    np.testing.assert_array_equal(res["1"][0], want_c)
+    np.testing.assert_array_equal(res["1"][1], want_s)
