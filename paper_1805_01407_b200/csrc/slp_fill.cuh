@@ -1,0 +1,513 @@
+// Kernels K2/K3: step + scramble + convert + store (k_fill) and its launchers.
+#pragma once
+
+#include "slp_gen.cuh"
+
+namespace slp {
+namespace dev {
+
+// ---- K2/K3: fill ---------------------------------------------------------------
+//
+// A warp owns 32 consecutive substreams ("unit"); lane l keeps substream
+// u*32+l in registers.  Outputs are produced in tiles of 32 substreams x
+// row_bytes (= segs x 128 B, FillShape) per substream; CH = row_bytes / ES
+// outputs per substream per tile.  MODE:
+//   FILL_TMA     stream-major.  Every output pair goes to the warp's
+//                shared-memory tile as it is produced (STS.128,
+//                conflict-free under the 128B swizzle), and the full tile
+//                leaves with one 3-D TMA bulk tensor store
+//                (cp.async.bulk.tensor.3d, SASS UTMASTG) that writes
+//                row_bytes contiguous bytes of each of the 32 rows.  The
+//                row piece is >= 256 B because HBM absorbs a column sweep of
+//                64/128-byte pieces at only ~4.5-4.8 TB/s (profiles/wpattern.cu).
+//                With B buffers per warp, store i-B must have finished reading
+//                before tile i overwrites its buffer (cp.async.bulk.wait_group.read).
+//   FILL_STAGED  stream-major, same staging, element stores (any pitch/alignment);
+//   FILL_POS     position-major: each output is one coalesced warp store
+//                (any pitch/alignment);
+//   FILL_POS_TMA position-major through the same per-warp tile, laid out
+//                [position][lane]: one 2-D TMA store writes CH rows of the
+//                output x 32 consecutive substreams (256 B for u64).  Direct
+//                stores leave 256-byte pieces scattered over CH rows that
+//                are 8 MiB apart and ran at 2.5-5.5 TB/s.
+// Shared-memory tile layout [seg][row][128 B], chunk q of (seg, row) at
+// ((seg*32 + row) * 128) + ((q ^ (row & 7)) << 4)  (CU_TENSOR_MAP_SWIZZLE_128B).
+
+enum { FILL_TMA = 0, FILL_STAGED = 1, FILL_POS = 2, FILL_POS_TMA = 3 };
+constexpr int kFillThreads = kFillWarps * 32;
+
+// Fill tile configurations (slp_ops.h):
+//   segs x 128 B row pieces per TMA store, bufs tile buffers per warp;
+//   pre: with one buffer, the first `pre` 16-byte chunks of tile i are
+//     generated into registers while the TMA store of tile i-1 still reads
+//     the buffer, so the wait for it overlaps generation;
+//   unroll: outputs per sub-block; the tile is generated in a rolled loop
+//     of sub-blocks, because fully unrolled 1 KiB tiles of the 8- and 16-word
+//     generators overflow the 32 KB L1.5 instruction cache.
+struct FillCfg {
+  int segs, bufs, pre, unroll;
+};
+// (a switch, not an array: namespace-scope constexpr arrays are host-only in CUDA)
+__host__ __device__ constexpr FillCfg fill_cfg_at(int i) {
+  switch (i) {
+    case 1: return FillCfg{8, 1, 16, 64};
+    case 2: return FillCfg{8, 1, 16, 128};
+    case 3: return FillCfg{4, 2, 0, 32};  // 512 B rows, two buffers
+    case 4: return FillCfg{4, 2, 0, 64};
+    default: return FillCfg{8, 1, 16, 32};  // 0: 1 KiB rows, one buffer
+  }
+}
+constexpr int kNumFillCfgs = 5;
+enum { FILL_KIND_NATIVE = 0, FILL_KIND_CONVERT = 1, FILL_KIND_CHECKSUM = 2 };
+}  // namespace dev
+}  // namespace slp
+#include "slp_fill_tuning.h"  // fill_tune(generator id, kind) -> configuration index (measured)
+namespace slp {
+namespace dev {
+
+// -DSLP_FILL_CFG=i forces configuration i for every kernel (tuning builds,
+// profiles/tune_fill.py)
+__host__ __device__ constexpr FillCfg fill_cfg(int id, int kind) {
+#ifdef SLP_FILL_CFG
+  return (void)id, (void)kind, fill_cfg_at(SLP_FILL_CFG);
+#else
+  return fill_cfg_at(fill_tune(id, kind));
+#endif
+}
+
+template <class G, int KIND>
+struct FillShape {
+  static constexpr FillCfg cfg = fill_cfg(G::id, KIND);
+  static constexpr int segs = cfg.segs, bufs = cfg.bufs, pre = cfg.pre, unroll = cfg.unroll;
+  static constexpr int row_bytes = segs * 128;
+  static constexpr int tile_bytes = 32 * row_bytes;
+  static constexpr int smem = kFillWarps * bufs * tile_bytes + 1024;
+  static_assert(smem <= 227 * 1024, "fill tiles exceed shared memory");
+};
+
+template <int OK, bool CSUM>
+__host__ __device__ constexpr int fill_kind() {
+  return CSUM ? FILL_KIND_CHECKSUM : (OK == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT);
+}
+
+__host__ __device__ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+
+__device__ __forceinline__ uint32_t swz(int seg, int r, int q) { return ((seg * 32 + r) << 7) + ((q ^ (r & 7)) << 4); }
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+               :
+               : "l"(reinterpret_cast<uint64_t>(map)), "r"(src), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
+// CSUM: also reduce the integer outputs while storing them (wrapping sum,
+// xor, exact sum and low-bit sum, as k_fused) -- "store mode plus fused
+// checksum" of BASELINE config 3 in one pass; partials go to p.partials.
+// exact per-CTA reduction of checksum accumulators into partials[blockIdx.x]
+template <int WPB>
+__device__ __forceinline__ void reduce_checksum_block(uint64_t slo, uint64_t shi, uint64_t sx, uint64_t slow,
+                                                      double fs, void *partials) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const uint64_t olo = __shfl_xor_sync(0xffffffffu, slo, off);
+    const uint64_t ohi = __shfl_xor_sync(0xffffffffu, shi, off);
+    const uint64_t nlo = slo + olo;
+    shi = shi + ohi + (nlo < slo ? 1 : 0);
+    slo = nlo;
+    sx ^= __shfl_xor_sync(0xffffffffu, sx, off);
+    slow += __shfl_xor_sync(0xffffffffu, slow, off);
+    fs += __shfl_xor_sync(0xffffffffu, fs, off);
+  }
+  __shared__ uint64_t r_lo[WPB], r_hi[WPB], r_x[WPB], r_low[WPB];
+  __shared__ double r_fs[WPB];
+  if (lane == 0) {
+    r_lo[warp] = slo;
+    r_hi[warp] = shi;
+    r_x[warp] = sx;
+    r_low[warp] = slow;
+    r_fs[warp] = fs;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t lo = 0, hi = 0, x = 0, low = 0;
+    double f = 0.0;
+    for (int i = 0; i < WPB; ++i) {
+      const uint64_t nlo = lo + r_lo[i];
+      hi += r_hi[i] + (nlo < lo ? 1 : 0);
+      lo = nlo;
+      x ^= r_x[i];
+      low += r_low[i];
+      f += r_fs[i];
+    }
+    slp_checksum *part = static_cast<slp_checksum *>(partials) + blockIdx.x;
+    part->sum_lo = lo;
+    part->sum_hi = hi;
+    part->xor_all = x;
+    part->low_sum = low;
+    part->count = 0;
+    part->fsum = f;
+  }
+}
+
+template <class G, int OK, int MODE, bool CSUM = false>
+__global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __grid_constant__ CUtensorMap tmap) {
+  using word = typename G::word;
+  using Cv = Out<OK, word>;
+  using bits = typename Cv::bits;
+  constexpr int K = G::k;
+  constexpr int ES = sizeof(bits);
+  using Shape = FillShape<G, fill_kind<OK, CSUM>()>;
+  constexpr int kFillBufs = Shape::bufs, kSegs = Shape::segs, kTileBytes = Shape::tile_bytes;
+  constexpr int CH = Shape::row_bytes / ES;                       // outputs per substream per tile
+  constexpr int EPC = 16 / ES;                                    // elements per 16-byte chunk
+  constexpr int U = Shape::unroll < CH ? Shape::unroll : CH;       // outputs per sub-block
+  static_assert(CH % U == 0 && U % EPC == 0 && (U * ES) % 128 == 0, "sub-blocks must be whole 128-byte segments");
+  static_assert(!G::ring || U % K == 0, "sub-blocks must cover whole ring periods");
+  // 16-byte chunks produced before the buffer wait (at most one sub-block)
+  constexpr int PRE = MODE == FILL_POS ? 0 : (Shape::pre * EPC <= U ? Shape::pre : U / EPC);
+  constexpr int MSK = G::best_mask(0, 0);  // rotation pipe mix (ALU vs FMA), see Gen::best_mask
+  const int lane = threadIdx.x & 31;
+  const int warp = warp_uniform();  // keeps TMA coordinates in uniform registers
+
+  extern __shared__ uint8_t smem_raw[];
+  uint32_t tiles = 0;
+  if constexpr (MODE != FILL_POS)
+    tiles = ((smem_u32(smem_raw) + 1023u) & ~1023u) + warp * kFillBufs * kTileBytes;  // 128B-swizzle atoms: 1 KiB
+
+  const word *__restrict__ sin = static_cast<const word *>(p.sin);
+  word *sout = static_cast<word *>(p.sout);
+  bits *__restrict__ out = static_cast<bits *>(p.out);
+  const uint64_t ntiles = p.T / CH;
+  const uint64_t rem = p.T - ntiles * CH;
+  uint32_t issued = 0;  // tiles produced by this warp
+  uint64_t cs_lo = 0, cs_hi = 0, cs_x = 0, cs_low = 0;  // CSUM accumulators (zero states emit zeros)
+
+  // the next unit's start states are loaded while this unit is generated
+  // (the load latency otherwise stalls every warp at each unit start)
+  const uint64_t ustride = (uint64_t)gridDim.x * kFillWarps;
+  auto load_states = [&](uint64_t unit, word(&dst)[K]) {
+    const uint64_t st = unit * 32 + lane;
+    const bool ok = unit < p.nunits && st < p.nstreams;
+#pragma unroll
+    for (int j = 0; j < K; ++j) dst[j] = ok ? sin[j * p.ld + st] : (word)0;
+  };
+  word nxt[K];
+  load_states((uint64_t)blockIdx.x * kFillWarps + warp, nxt);
+  for (uint64_t u = (uint64_t)blockIdx.x * kFillWarps + warp; u < p.nunits; u += ustride) {
+    const uint64_t row0 = u * 32;
+    const uint64_t stream = row0 + lane;
+    const bool valid = stream < p.nstreams;
+    word s[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) s[j] = nxt[j];
+    load_states(u + ustride, nxt);
+
+    for (uint64_t c = 0; c < ntiles; ++c) {
+      const uint64_t pos0 = c * CH;
+      uint32_t tile = 0;
+      auto wait_buffer = [&] {
+        if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA) {
+          if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
+        }
+        __syncwarp();
+      };
+      // one 16-byte chunk (outputs b+e .. b+e+EPC-1 of this lane's row) into the
+      // tile; b (runtime) is a sub-block start, e (compile time) the offset in it
+      auto put = [&](uint32_t b, int e, const bits(&v)[EPC]) {
+        if constexpr (MODE == FILL_POS_TMA) {  // tile [position][lane]
+          const uint32_t row = tile + (b * 32 + lane) * ES;
+#pragma unroll
+          for (int i = 0; i < EPC; ++i) {
+            const uint32_t addr = row + (e + i) * 32 * ES;
+            if constexpr (ES == 8)
+              asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"((uint64_t)v[i]) : "memory");
+            else
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"((uint32_t)v[i]) : "memory");
+          }
+          return;
+        }
+        const int byte = e * ES;
+        const uint32_t addr = tile + ((b * ES / 128) << 12) + swz(byte >> 7, lane, (byte & 127) >> 4);
+        if constexpr (ES == 8) {
+          asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(addr), "l"((uint64_t)v[0]), "l"((uint64_t)v[1])
+                       : "memory");
+        } else {
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"((uint32_t)v[0]),
+                       "r"((uint32_t)v[1]), "r"((uint32_t)v[2]), "r"((uint32_t)v[3])
+                       : "memory");
+        }
+      };
+      // EPC outputs at sub-block offset e (ring offset (e + i) % K is static since U % K == 0)
+      // CSUM, per tile: sums of the 32-bit halves (exact in 64 bits), xor and
+      // low-bit sum, one chunk at a time (3-input adds / LOP3 over the chunk)
+      uint64_t t_lo = 0, t_hi = 0;
+      word t_x = 0;
+      uint32_t t_low = 0;
+      auto gen = [&](int e, bits(&v)[EPC]) {
+        word rr[EPC];
+#pragma unroll
+        for (int i = 0; i < EPC; ++i) {
+          const int o = (e + i) % K;
+          rr[i] = G::template output_m<MSK>(s, o);
+          v[i] = Cv::conv(rr[i]);
+          G::template step_m<MSK>(s, o);
+        }
+        if constexpr (CSUM) {
+          constexpr uint32_t LOWM = G::w == 64 ? 0x7FFu : 0xFFu;
+          word x = rr[0];
+          uint32_t lw = (uint32_t)rr[0] & LOWM;
+          uint64_t slo = (uint32_t)rr[0], shi = (uint64_t)rr[0] >> 32;
+#pragma unroll
+          for (int i = 1; i < EPC; ++i) {
+            x ^= rr[i];
+            lw += (uint32_t)rr[i] & LOWM;
+            slo += (uint32_t)rr[i];
+            shi += (uint64_t)rr[i] >> 32;
+          }
+          t_x ^= x;
+          t_low += lw;
+          t_lo += slo;
+          if constexpr (G::w == 64) t_hi += shi;
+        }
+      };
+      auto emit = [&](uint32_t b, int e, const bits(&v)[EPC]) {
+        if constexpr (MODE == FILL_POS) {
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < EPC; ++i) out[(pos0 + b + e + i) * p.ld_out + stream] = v[i];
+          }
+        } else {
+          put(b, e, v);
+        }
+      };
+      if constexpr (MODE != FILL_POS) {
+        tile = tiles + (issued % kFillBufs) * kTileBytes;
+        if constexpr (PRE == 0) wait_buffer();
+      }
+      // sub-block 0, peeled: its first PRE chunks are produced while the
+      // buffer's previous TMA store is still reading it
+      bits hold[PRE > 0 ? PRE : 1][EPC];
+#pragma unroll
+      for (int e = 0; e < U; e += EPC) {
+        bits v[EPC];
+        gen(e, v);
+        if (e < PRE * EPC) {
+#pragma unroll
+          for (int i = 0; i < EPC; ++i) hold[e / EPC][i] = v[i];
+          if (e == (PRE - 1) * EPC) {
+            wait_buffer();
+#pragma unroll
+            for (int q = 0; q < PRE; ++q) put(0, q * EPC, hold[q]);
+          }
+        } else {
+          emit(0, e, v);
+        }
+      }
+      // remaining sub-blocks: a rolled loop keeps the body within the
+      // instruction cache (a fully unrolled 1 KiB-row tile of an 8-word
+      // generator is ~60 KB of SASS, twice the 32 KB L1.5 I-cache)
+#pragma unroll 1
+      for (uint32_t b = U; b < (uint32_t)CH; b += U) {
+#pragma unroll
+        for (int e = 0; e < U; e += EPC) {
+          bits v[EPC];
+          gen(e, v);
+          emit(b, e, v);
+        }
+      }
+      if constexpr (CSUM) {
+        add128(cs_lo, cs_hi, t_lo);
+        add128(cs_lo, cs_hi, t_hi << 32);
+        cs_hi += t_hi >> 32;
+        cs_x ^= (uint64_t)t_x;
+        cs_low += t_low;
+      }
+      if constexpr (MODE == FILL_TMA) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (elect_one()) {
+          tma_store_3d(&tmap, tile, 0, (int)row0, (int)(pos0 * ES / 128));
+          bulk_commit();
+        }
+        ++issued;
+      } else if constexpr (MODE == FILL_POS_TMA) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (elect_one()) {
+          tma_store_2d(&tmap, tile, (int)row0, (int)pos0);
+          bulk_commit();
+        }
+        ++issued;
+      } else if constexpr (MODE == FILL_STAGED) {
+        __syncwarp();
+        // element stores; CPR lanes cover one 128-byte segment of a row
+        constexpr int CPR = 128 / ES;  // elements per segment
+        constexpr int RPP = 32 / CPR;  // rows per pass (1 for u32, 2 for u64)
+#pragma unroll 4
+        for (int r0 = 0; r0 < 32 * kSegs; r0 += RPP) {
+          const int rs = r0 + lane / CPR;  // (seg, row) flattened seg-major
+          const int seg = rs / 32, r = rs % 32;
+          const int e = lane % CPR;
+          const uint64_t srow = row0 + r;
+          bits v;
+          const uint32_t addr = tile + swz(seg, r, (e * ES) >> 4) + (e * ES & 15);
+          if constexpr (ES == 8) {
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+          } else {
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+          }
+          if (srow < p.nstreams) out[srow * p.ld_out + pos0 + seg * CPR + e] = v;
+        }
+        __syncwarp();
+        ++issued;
+      }
+    }
+    for (uint64_t t = 0; t < rem; ++t) {
+      const word r = G::next_flat(s);
+      const bits x = Cv::conv(r);
+      if constexpr (CSUM) {
+        add128(cs_lo, cs_hi, (uint64_t)r);
+        cs_x ^= (uint64_t)r;
+        cs_low += (uint32_t)r & (G::w == 64 ? 0x7FFu : 0xFFu);
+      }
+      if (valid) {
+        const uint64_t pos = ntiles * CH + t;
+        if constexpr (MODE == FILL_POS || MODE == FILL_POS_TMA)
+          out[pos * p.ld_out + stream] = x;
+        else
+          out[stream * p.ld_out + pos] = x;
+      }
+    }
+    if (valid && sout) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) sout[j * p.ld + stream] = s[j];
+    }
+  }
+  if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA) {
+    if (elect_one()) bulk_wait_all<0>();
+  }
+  if constexpr (CSUM) reduce_checksum_block<kFillWarps>(cs_lo, cs_hi, cs_x, cs_low, 0.0, p.partials);
+}
+
+
+// ---- host launchers ----------------------------------------------------------------
+
+template <class G, int OK, int MODE, bool CSUM = false>
+int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) {
+  using bits = typename Out<OK, typename G::word>::bits;
+  constexpr int ES = sizeof(bits);
+  FillParams p = p0;
+  if (grid_out) *grid_out = 0;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof tmap);
+  if constexpr (MODE == FILL_TMA) {
+    int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, FillShape<G, fill_kind<OK, CSUM>()>::segs);
+    if (rc != SLP_OK) return rc;
+  } else if constexpr (MODE == FILL_POS_TMA) {
+    int rc = make_store_tmap_pm(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out,
+                                FillShape<G, fill_kind<OK, CSUM>()>::row_bytes / ES);
+    if (rc != SLP_OK) return rc;
+  }
+  auto kern = k_fill<G, OK, MODE, CSUM>;
+  const int smem = MODE == FILL_POS ? 0 : FillShape<G, fill_kind<OK, CSUM>()>::smem;
+  p.nunits = (p.nstreams + 31) / 32;
+  const int dev = current_device();
+  static std::atomic<int> per_sm[64];  // occupancy per device, computed once (benign race: same value)
+  if (dev < 0 || dev >= 64) return SLP_ERR_CUDA;
+  if (!per_sm[dev]) {
+    if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return cuda_fail("cudaFuncSetAttribute");
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kFillThreads, smem) != cudaSuccess || b < 1)
+      return cuda_fail("occupancy");
+    per_sm[dev] = b;
+  }
+  if (p.nunits == 0 || p.T == 0) return SLP_OK;
+  uint64_t want = (p.nunits + kFillWarps - 1) / kFillWarps;
+  uint64_t cap = (uint64_t)sm_count(dev) * per_sm[dev] * fill_grid_mult();
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  if constexpr (CSUM) {
+    if ((uint64_t)grid * sizeof(slp_checksum) > p.workspace_bytes) return SLP_ERR_BUFFER;
+  }
+  if (grid_out) *grid_out = (int)grid;
+  kern<<<grid, kFillThreads, smem, st>>>(p, tmap);
+  return check_launch("k_fill");
+}
+
+// store + checksum in one pass: stream-major TMA path only (else UNSUPPORTED;
+// callers fall back to a fill followed by a fused pass over the same states)
+template <class G>
+int fill_csum_impl(const FillParams &p, int out_kind, cudaStream_t st, int *grid_out) {
+  constexpr int W = G::w;
+  if (grid_out) *grid_out = 0;
+  int ok;
+  if (out_kind == SLP_OUT_NATIVE || (out_kind == SLP_OUT_U64 && W == 64))
+    ok = SLP_OUT_NATIVE;
+  else if (out_kind == SLP_OUT_F64 && W == 64)
+    ok = SLP_OUT_F64;
+  else if (out_kind == SLP_OUT_F32 && W == 32)
+    ok = SLP_OUT_F32;
+  else
+    return SLP_ERR_UNSUPPORTED;
+  const int es = ok == SLP_OUT_NATIVE ? W / 8 : (ok == SLP_OUT_F32 ? 4 : 8);
+  if (!tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, fill_cfg(G::id, FILL_KIND_CHECKSUM).segs))
+    return SLP_ERR_UNSUPPORTED;
+  if constexpr (W == 64) {
+    if (ok == SLP_OUT_F64) return launch_fill<G, SLP_OUT_F64, FILL_TMA, true>(p, st, grid_out);
+  } else {
+    if (ok == SLP_OUT_F32) return launch_fill<G, SLP_OUT_F32, FILL_TMA, true>(p, st, grid_out);
+  }
+  return launch_fill<G, SLP_OUT_NATIVE, FILL_TMA, true>(p, st, grid_out);
+}
+
+template <class G>
+int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
+  constexpr int W = G::w;
+  int ok;
+  if (out_kind == SLP_OUT_NATIVE || (out_kind == SLP_OUT_U64 && W == 64))
+    ok = SLP_OUT_NATIVE;
+  else if (out_kind == SLP_OUT_U64)
+    ok = SLP_OUT_U64;
+  else if (out_kind == SLP_OUT_F64 && W == 64)
+    ok = SLP_OUT_F64;
+  else if (out_kind == SLP_OUT_F32 && W == 32)
+    ok = SLP_OUT_F32;
+  else
+    return SLP_ERR_UNSUPPORTED;
+  const int es = (ok == SLP_OUT_NATIVE) ? W / 8 : (ok == SLP_OUT_F32 ? 4 : 8);
+  int mode;
+  if (layout == SLP_POSITION_MAJOR)
+    mode = tma_ok_pm(p.out, es, p.T, p.nstreams, p.ld_out,
+                     fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs * 128 / es)
+               ? FILL_POS_TMA
+               : FILL_POS;
+  else if (layout == SLP_STREAM_MAJOR)
+    mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out,
+                  fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs)
+               ? FILL_TMA
+               : FILL_STAGED;
+  else
+    return SLP_ERR_INVALID;
+#define SLP_FILL_CASE(OKV)                                                     \
+  if (ok == OKV) {                                                             \
+    if (mode == FILL_TMA) return launch_fill<G, OKV, FILL_TMA>(p, st);         \
+    if (mode == FILL_STAGED) return launch_fill<G, OKV, FILL_STAGED>(p, st);   \
+    if (mode == FILL_POS_TMA) return launch_fill<G, OKV, FILL_POS_TMA>(p, st); \
+    return launch_fill<G, OKV, FILL_POS>(p, st);                               \
+  }
+  if constexpr (W == 64) {
+    SLP_FILL_CASE(SLP_OUT_NATIVE)
+    SLP_FILL_CASE(SLP_OUT_F64)
+  } else {
+    SLP_FILL_CASE(SLP_OUT_NATIVE)
+    SLP_FILL_CASE(SLP_OUT_U64)
+    SLP_FILL_CASE(SLP_OUT_F32)
+  }
+#undef SLP_FILL_CASE
+  return SLP_ERR_UNSUPPORTED;
+}
+
+}  // namespace dev
+}  // namespace slp

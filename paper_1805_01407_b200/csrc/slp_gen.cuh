@@ -1,0 +1,401 @@
+// Device building blocks for the scrambled linear generators on sm_100a:
+// word operations, the Gen<> template (engine step + scrambler), output
+// conversions and PTX helpers.  Kernels: slp_fill.cuh (K2/K3), slp_fused.cuh
+// (K4), slp_jump.cuh (K1, K1t), slp_hwd.cuh (K6); slp_device.cuh includes all.
+//
+// One template instance per registry generator (slp_registry.h): the whole
+// state lives in registers in FLAT word order (engines.py:14-18).  The cyclic
+// engines (xoroshiro, incl. the 16-word ring of xoroshiro1024, and xorshift)
+// are stepped as a register ring whose offset is a compile-time constant
+// inside fully unrolled chunks of a multiple of k steps, so the reference's
+// ring pointer (generators.py:260-274) costs nothing at run time.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <type_traits>
+
+#include "../../include/slp_b200.h"
+#include "slp_ops.h"
+#include "slp_registry.h"
+
+namespace slp {
+namespace dev {
+
+template <int W>
+struct WordOf;
+template <>
+struct WordOf<64> {
+  using type = uint64_t;
+};
+template <>
+struct WordOf<32> {
+  using type = uint32_t;
+};
+
+// PTX wide multiply-adds: ptxas keeps these on the FMA pipe (IMAD.WIDE.U32 /
+// IMAD), even for power-of-two multipliers, which is how shifts and rotations
+// are moved off the ALU pipe below.
+__device__ __forceinline__ uint64_t mulw(uint32_t a, uint32_t b) {
+  uint64_t d;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t madw(uint32_t a, uint32_t b, uint64_t c) {
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// Word operations.  64-bit words are manipulated as explicit 32-bit halves.
+// The generators are integer-issue bound on the ALU pipe (LOP3/SHF/IADD3,
+// profiles/).  Measured on sm_100 (profiles/int_peak.cu): LOP3, SHF and IMAD
+// issue at 2 per SM per cycle, IMAD.HI at 1, IMAD.WIDE at 0.5.  Hence:
+//   rotl   : two funnel shifts (SHF.L.W)                 -> 2 ALU  (default)
+//   rotl_f : three wide multiply-adds by 2^r             -> 3 FMA  (A/B only:
+//            Gen::best_mask with SLP_ROT_POLICY=1 loses to IMAD.WIDE's rate)
+//   shl    : IMAD.SHL (low half) + SHF.L.U64.HI          -> 1 FMA + 1 ALU
+//   mulc   : IMAD.WIDE + IMAD (+ IMAD for a 64-bit constant).
+#ifndef SLP_MUL_POLICY
+#define SLP_MUL_POLICY 1  // 0: shifts via IMAD.WIDE; 1: 64-bit constant shifts as IMAD.SHL + SHF; 2: also x*(2^a+1) as LEA pairs
+#endif
+
+template <int W>
+struct WOps;
+
+template <>
+struct WOps<32> {
+  using word = uint32_t;
+  template <int R>
+  static __device__ __forceinline__ word rotl(word x) {
+    return __funnelshift_l(x, x, R);
+  }
+  template <int R>
+  static __device__ __forceinline__ word rotl_f(word x) {
+    return __funnelshift_l(x, x, R);  // no cheaper FMA form for one 32-bit word
+  }
+  template <int B>
+  static __device__ __forceinline__ word shl(word x) {
+    return x << B;
+  }
+  template <int B>
+  static __device__ __forceinline__ word shr(word x) {
+    return x >> B;
+  }
+  template <unsigned long long C>
+  static __device__ __forceinline__ word mulc(word x) {
+    return x * (uint32_t)C;
+  }
+};
+
+template <>
+struct WOps<64> {
+  using word = uint64_t;
+  static __device__ __forceinline__ uint32_t lo(word x) { return (uint32_t)x; }
+  static __device__ __forceinline__ uint32_t hi(word x) { return (uint32_t)(x >> 32); }
+  static __device__ __forceinline__ word pack(uint32_t l, uint32_t h) { return ((uint64_t)h << 32) | l; }
+  template <int R>
+  static __device__ __forceinline__ word rotl(word x) {
+    uint32_t l = lo(x), h = hi(x);
+    if constexpr (R >= 32) {
+      const uint32_t t = l;
+      l = h;
+      h = t;
+    }
+    constexpr int r = R & 31;
+    if constexpr (r == 0) return pack(l, h);
+    return pack(__funnelshift_l(h, l, r), __funnelshift_l(l, h, r));
+  }
+  template <int R>
+  static __device__ __forceinline__ word rotl_f(word x) {
+    uint32_t l = lo(x), h = hi(x);
+    if constexpr (R >= 32) {
+      const uint32_t t = l;
+      l = h;
+      h = t;
+    }
+    constexpr int r = R & 31;
+    if constexpr (r == 0) return pack(l, h);
+    constexpr uint32_t m = 1u << r;
+    const uint64_t w1 = mulw(l, m);                          // (l << r, l >> (32 - r))
+    const uint64_t w2 = madw(h, m, w1 >> 32);                // low: (h << r) | (l >> (32 - r))
+    const uint64_t w3 = madw(l, m, w2 >> 32);                // low: (l << r) | (h >> (32 - r))
+    return pack((uint32_t)w3, (uint32_t)w2);
+  }
+  template <int B>
+  static __device__ __forceinline__ word shl(word x) {
+#if SLP_MUL_POLICY >= 1
+    // IMAD.SHL (lo) + SHF.L.U64.HI (hi): IMAD.WIDE issues at a quarter of the
+    // IMAD rate on sm_100 (profiles/int_peak.cu)
+    return x << B;
+#else
+    if constexpr (B >= 32) return pack(0u, lo(x) << (B - 32));
+    const uint64_t w = mulw(lo(x), 1u << B);
+    return pack((uint32_t)w, madlo(hi(x), 1u << B, (uint32_t)(w >> 32)));
+#endif
+  }
+  template <int B>
+  static __device__ __forceinline__ word shr(word x) {
+    if constexpr (B >= 32) return pack(hi(x) >> (B - 32), 0u);
+    return pack(__funnelshift_r(lo(x), hi(x), B), hi(x) >> B);
+  }
+  template <unsigned long long C>
+  static __device__ __forceinline__ word mulc(word x) {
+#if SLP_MUL_POLICY == 2
+    // 2^a + 1 (the ** constants 5 and 9): x + (x << a) = LEA + LEA.HI.X, which
+    // issue at up to twice the single-pipe rate, instead of IMAD.WIDE + IMAD
+    constexpr int a = (C > 1 && ((C - 1) & (C - 2)) == 0) ? __builtin_ctzll(C - 1) : -1;
+    if constexpr (a > 0 && a < 32) return x + (x << a);
+#endif
+    const uint64_t p = mulw(lo(x), (uint32_t)C);
+    uint32_t h = madlo(hi(x), (uint32_t)C, (uint32_t)(p >> 32));
+    if constexpr ((C >> 32) != 0) h = madlo(lo(x), (uint32_t)(C >> 32), h);
+    return pack((uint32_t)p, h);
+  }
+};
+
+// Build-time policy switches (A/B experiments, profiles/): rotation pipe
+// balancing and the fused accumulator form.
+#ifndef SLP_ROT_POLICY
+#define SLP_ROT_POLICY 0  // 0: all rotations on the ALU; 1: Gen::best_mask (A/B: no gain, ptxas re-normalises)
+#endif
+#ifndef SLP_SUM_POLICY
+#define SLP_SUM_POLICY 3  // 0: 128-bit carry chain per output; 1, 2: IMAD.WIDE accumulators; 3: half sums
+#endif
+
+// Pipe cost of one output, in warp instructions per 32 outputs
+struct PipeCost {
+  int alu, fma;
+};
+
+template <int ID, int FAM, int K, int W, int A, int B, int C, int SC, int WI, int WJ, unsigned long long S_, int R_,
+          unsigned long long T_>
+struct Gen {
+  static constexpr int id = ID;  // registry id (slp_registry.h)
+  using word = typename WordOf<W>::type;
+  using O = WOps<W>;
+  static constexpr int k = K;
+  static constexpr int w = W;
+  static constexpr int n = K * W;
+  static constexpr int pw = n / 64;  // u64 words per jump polynomial (degree < n)
+  static constexpr bool ring = FAM != SLP_FAM_XOSHIRO;
+  static constexpr int sc = SC;
+  static constexpr int fam = FAM;
+
+  // Rotation sites that may run on either pipe (bit set in a mask = FMA form):
+  //   bit 0: engine rotation by A (xoroshiro) / by B (xoshiro)
+  //   bit 1: engine rotation by C (xoroshiro)
+  //   bit 2: scrambler rotation by R (++ and **)
+  static constexpr int kSites = (W == 64 ? ((FAM == SLP_FAM_XOROSHIRO ? 3 : (FAM == SLP_FAM_XOSHIRO ? 1 : 0)) |
+                                            ((SC == SLP_SC_PLUSPLUS || SC == SLP_SC_STARSTAR) ? 4 : 0))
+                                         : 0);
+
+  // ALU/FMA instructions per output outside the rotation sites (SASS counts, profiles/)
+  static __host__ __device__ constexpr PipeCost fixed() {
+    PipeCost c{0, 0};
+    const int h = W == 64 ? 2 : 1;  // 32-bit halves per word
+    if (FAM == SLP_FAM_XOROSHIRO) {
+      c.alu += 2 * h;               // xl = s[l] ^ s0; new = rot ^ xl ^ shl (3-input LOP3)
+      c.fma += W == 64 ? 2 : 1;     // xl << B
+    } else if (FAM == SLP_FAM_XORSHIFT) {
+      c.alu += 5 * h;
+      c.fma += 2;
+    } else {
+      c.alu += (K == 4 ? 4 : 7) * h;  // the xor network (LOP3 fuses pairs)
+      c.fma += W == 64 ? 2 : 1;       // t = s1 << A
+    }
+    if (W == 32) c.alu += FAM == SLP_FAM_XOROSHIRO ? 2 : 1;  // 32-bit rotations always on the ALU
+    if (SC == SLP_SC_PLUS) c.alu += h;
+    if (SC == SLP_SC_STAR) c.fma += W == 64 ? ((S_ >> 32) ? 3 : 2) : 1;
+    if (SC == SLP_SC_PLUSPLUS) c.alu += 2 * h + (W == 32 ? 1 : 0);
+    if (SC == SLP_SC_STARSTAR) c.fma += W == 64 ? 4 : 2, c.alu += W == 32 ? 1 : 0;
+    return c;
+  }
+  // best rotation mask given extra per-output work of the calling kernel
+  static __host__ __device__ constexpr int best_mask(int extra_alu, int extra_fma) {
+    if (SLP_ROT_POLICY == 0) return 0;
+    const PipeCost f = fixed();
+    int best = 0, best_cost = 1 << 30;
+    for (int m = 0; m < 8; ++m) {
+      if ((m & ~kSites) != 0) continue;
+      int alu = f.alu + extra_alu, fma = f.fma + extra_fma;
+      for (int bit = 0; bit < 3; ++bit) {
+        if (!(kSites & (1 << bit))) continue;
+        if (m & (1 << bit))
+          fma += 3;
+        else
+          alu += 2;
+      }
+      const int cost = (2 * alu > 2 * fma ? 2 * alu : 2 * fma) > alu + fma ? (2 * alu > 2 * fma ? 2 * alu : 2 * fma)
+                                                                            : alu + fma;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = m;
+      }
+    }
+    return best;
+  }
+
+  template <int M, int RR>
+  static __device__ __forceinline__ word rot(word x) {
+    if constexpr (M != 0)
+      return O::template rotl_f<RR>(x);
+    else
+      return O::template rotl<RR>(x);
+  }
+
+  // register slot of flat word j when the ring offset is o (constant after unrolling)
+  static __device__ __forceinline__ constexpr int slot(int o, int j) { return ring ? (o + j) % K : j; }
+
+  // scramblers.py:84-95, applied to the current (pre-step) state
+  template <int M>
+  static __device__ __forceinline__ word output_m(const word (&s)[K], int o) {
+    const word xi = s[slot(o, WI)];
+    if constexpr (SC == SLP_SC_NONE) {
+      return xi;
+    } else if constexpr (SC == SLP_SC_PLUS) {
+      return (word)(xi + s[slot(o, WJ)]);
+    } else if constexpr (SC == SLP_SC_STAR) {
+      return O::template mulc<S_>(xi);
+    } else if constexpr (SC == SLP_SC_PLUSPLUS) {
+      return (word)(rot<M & 4, R_>((word)(xi + s[slot(o, WJ)])) + xi);
+    } else {
+      return O::template mulc<T_>(rot<M & 4, R_>(O::template mulc<S_>(xi)));
+    }
+  }
+
+  // one engine step in the flat view (engines.py:100-140).  For ring engines
+  // the flat view moves by one slot: the caller's next offset is o + 1.
+  template <int M>
+  static __device__ __forceinline__ void step_m(word (&s)[K], int o) {
+    if constexpr (FAM == SLP_FAM_XOROSHIRO) {
+      const int i0 = slot(o, 0), il = slot(o, K - 1);
+      const word x0 = s[i0];
+      const word xl = s[il] ^ x0;
+      s[il] = rot<M & 1, A>(x0) ^ xl ^ O::template shl<B>(xl);
+      s[i0] = rot<M & 2, C>(xl);
+    } else if constexpr (FAM == SLP_FAM_XORSHIFT) {
+      const int i0 = slot(o, 0), i1 = slot(o, 1);
+      const word s0 = s[i0], s1 = s[i1];
+      const word t = s0 ^ O::template shl<A>(s0);
+      s[i0] = t ^ O::template shr<B>(t) ^ s1 ^ O::template shr<C>(s1);
+    } else if constexpr (K == 4) {
+      const word t = O::template shl<A>(s[1]);
+      s[2] ^= s[0];
+      s[3] ^= s[1];
+      s[1] ^= s[2];
+      s[0] ^= s[3];
+      s[2] ^= t;
+      s[3] = rot<M & 1, B>(s[3]);
+    } else {
+      const word t = O::template shl<A>(s[1]);
+      s[2] ^= s[0];
+      s[5] ^= s[1];
+      s[1] ^= s[2];
+      s[7] ^= s[3];
+      s[3] ^= s[4];
+      s[4] ^= s[5];
+      s[0] ^= s[6];
+      s[6] ^= s[7];
+      s[6] ^= t;
+      s[7] = rot<M & 1, B>(s[7]);
+    }
+  }
+
+  // defaults (all-ALU rotations): jump kernel and tails
+  static __device__ __forceinline__ word output(const word (&s)[K], int o) { return output_m<0>(s, o); }
+  static __device__ __forceinline__ void step(word (&s)[K], int o) { step_m<0>(s, o); }
+
+  // one output + step, registers left in flat order (tails of odd length)
+  static __device__ __forceinline__ word next_flat(word (&s)[K]) {
+    const word out = output(s, 0);
+    step(s, 0);
+    if constexpr (ring) {
+      const word first = s[0];
+#pragma unroll
+      for (int j = 0; j + 1 < K; ++j) s[j] = s[j + 1];
+      s[K - 1] = first;
+    }
+    return out;
+  }
+};
+
+// ---- output conversion (K3) ------------------------------------------------
+// bit patterns of the converted element; conversion is exact in both cases:
+// x >> 11 < 2^53 and x >> 8 < 2^24 are representable, the scale is a power of 2.
+
+template <int OK, class word>
+struct Out;
+template <class word>
+struct Out<SLP_OUT_NATIVE, word> {
+  using bits = word;
+  static __device__ __forceinline__ bits conv(word x) { return x; }
+};
+template <class word>
+struct Out<SLP_OUT_U64, word> {
+  using bits = uint64_t;
+  static __device__ __forceinline__ bits conv(word x) { return (uint64_t)x; }
+};
+template <class word>
+struct Out<SLP_OUT_F64, word> {
+  using bits = uint64_t;
+  static __device__ __forceinline__ bits conv(word x) {
+    return (uint64_t)__double_as_longlong(__ull2double_rn((uint64_t)x >> 11) * 0x1.0p-53);
+  }
+};
+template <class word>
+struct Out<SLP_OUT_F32, word> {
+  using bits = uint32_t;
+  static __device__ __forceinline__ bits conv(word x) {
+    return (uint32_t)__float_as_uint(__uint2float_rn((uint32_t)x >> 8) * 0x1.0p-24f);
+  }
+};
+
+// ---- PTX helpers -------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+               :
+               : "l"(reinterpret_cast<uint64_t>(map)), "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// warp index the compiler can prove warp-uniform (result of a shuffle from lane 0)
+__device__ __forceinline__ int warp_uniform() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+// one elected lane of a converged warp (elect.sync picks the same leader every time)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+// 128-bit accumulate of a 64-bit value
+__device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t x) {
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(lo), "+l"(hi) : "l"(x));
+}
+
+}  // namespace dev
+}  // namespace slp
