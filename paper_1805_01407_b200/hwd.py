@@ -4,7 +4,7 @@ Drop-in for the generator-driven entry point of the reference test
 (/root/reference/pkg/src/slprng/hwd.py): ``run_generator`` streams the
 generator's single output stream straight into kernel K6 (generate ->
 test value -> popcount -> trit -> signature -> per-signature count and
-weight sum, csrc/slp_device.cuh) without ever storing the outputs, and
+weight sum, csrc/slp_hwd.cuh) without ever storing the outputs, and
 evaluates at every doubling of consumed values exactly like ``run``
 (hwd.py:516-595).  The evaluation (Kronecker-power transform, erfc p-values,
 category compensation) is host code restating hwd.py:101-132 and :260-326

@@ -3,7 +3,7 @@
 Mirrors /root/reference/pkg/src/slprng/scramblers.py (``ScramblerSpec``
 :48-95 and ``scramble_*`` :26-45).  Scramblers read the state BEFORE the
 engine step; for ``++`` the first word is the one added back.  The device
-kernels implement the same functions in registers (csrc/slp_device.cuh,
+kernels implement the same functions in registers (csrc/slp_gen.cuh,
 ``Gen::output``).
 """
 
