@@ -464,32 +464,60 @@ class VecStepper:
             raise ValueError(f"states must be ({self.kind.k}, L) {_word_dtype(self.kind.w)}")
 
     def word(self, S, i: int):
-        return S[i]
+        return S[i]  # flat order is physical: no rolling offset (engines.py:302-303)
 
     def flat(self, S):
         return S
 
     def set_flat(self, S, flat):
-        S.copy_(flat)
+        if isinstance(S, np.ndarray):
+            S[...] = np.asarray(flat, dtype=S.dtype)
+        else:
+            S.copy_(flat)
         self.off = 0
 
+    def _host(self, S, op):
+        """The reference's numpy (k, L) uint64 arrays (engines.py:276-283):
+        run ``op`` on a device copy and write the result back in place."""
+        dt = _word_dtype(self.kind.w)
+        if S.ndim != 2 or S.shape[0] != self.kind.k:
+            raise ValueError(f"states must be a ({self.kind.k}, L) array")
+        D = torch.from_numpy(np.ascontiguousarray(S).astype(np.uint64 if dt == torch.uint64 else np.uint32))
+        D = D.to(require_cuda())
+        op(D)
+        S[...] = D.cpu().numpy().astype(S.dtype, copy=False)
+
     def step(self, S):
+        if isinstance(S, np.ndarray):
+            return self._host(S, self.step)
         self._check(S)
         L = S.shape[1]
         if self._scratch is None or self._scratch.shape[1] < L or self._scratch.device != S.device:
             self._scratch = torch.empty((1, L), dtype=S.dtype, device=S.device)
-        fill(self.spec, S.contiguous() if not S.is_contiguous() else S, 1, out=self._scratch[:, :L],
-             layout="position")
+        if S.is_contiguous():
+            fill(self.spec, S, 1, out=self._scratch[:, :L], layout="position")
+        else:  # K2 needs unit column stride: step a contiguous copy, then write it back
+            C = S.contiguous()
+            fill(self.spec, C, 1, out=self._scratch[:, :L], layout="position")
+            S.copy_(C)
 
     def advance(self, S, steps: int):
+        if isinstance(S, np.ndarray):
+            return self._host(S, lambda D: self.advance(D, steps))
         self._check(S)
         if steps == 0:
             return
         jp = compute_jump_poly(self.spec, steps)
         pw, pn = _native.int_to_words(jp.poly.bits)
+        if S.stride(1) != 1:
+            C = S.contiguous()
+            self.advance(C, steps)
+            S.copy_(C)
+            return
         ptr = ctypes.c_void_p(S.data_ptr())
         L = S.shape[1]
+        ld = S.stride(0) if S.shape[0] > 1 else L
         with torch.cuda.device(S.device):
-            rc = _native.lib().slp_jump_states(native_id(self.spec), pw, pn, ptr, L, ptr, L, L,
+            rc = _native.lib().slp_jump_states(native_id(self.spec), pw, pn, ptr, ld, ptr, ld, L,
                                                _stream_ptr(S.device))
         _native.check(rc, "advance")

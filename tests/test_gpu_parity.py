@@ -409,3 +409,41 @@ def test_laned_fill_c_abi_superbatch(name):
     assert L.slp_fill(gid, sp, sp, lanes, lanes, lane_len, _native.OUT_U64, _native.STREAM_MAJOR,
                       ctypes.c_void_p(out.data_ptr()), lane_len, st) == 0
     np.testing.assert_array_equal(out.cpu().numpy().reshape(-1), want[lanes * lane_len:])
+
+
+@pytest.mark.parametrize("name", ["xoroshiro128plus", "xoshiro128starstar", "xoroshiro1024plusplus"])
+def test_vecstepper_numpy_and_strided_states(name):
+    """Drop-in use with the reference's numpy (k, L) uint64 arrays (also for
+    w = 32, engines.py:276-283), and column-sliced CUDA views."""
+    import random
+
+    spec = P.get_spec(name)
+    kind, params = spec.kind, spec.params
+    rng = random.Random(5)
+    states = [P.bits_to_words(rng.randrange(1, 1 << kind.n), kind.k, kind.w) for _ in range(7)]
+    want = [tuple(s) for s in states]
+    for _ in range(10):
+        want = [P.step(kind, params, s) for s in want]
+    # numpy uint64 host array, stepped in place
+    S = np.array(list(zip(*states)), dtype=np.uint64)
+    st = D.VecStepper(kind, params)
+    for _ in range(10):
+        st.step(S)
+    assert S.dtype == np.uint64
+    assert [tuple(int(v) for v in S[:, j]) for j in range(7)] == want
+    S2 = np.array(list(zip(*states)), dtype=np.uint64)
+    st.advance(S2, 10)
+    np.testing.assert_array_equal(S2, S)
+    # a column slice of a wider CUDA tensor (row pitch != L)
+    npdt = np.uint64 if kind.w == 64 else np.uint32
+    big = torch.zeros((kind.k, 20), dtype=torch.uint64 if kind.w == 64 else torch.uint32, device="cuda")
+    big[:, 3:10] = torch.from_numpy(np.array(list(zip(*states)), dtype=npdt)).cuda()
+    view = big[:, 3:10]
+    for _ in range(10):
+        st.step(view)
+    np.testing.assert_array_equal(view.cpu().numpy().astype(np.uint64), S)
+    big2 = torch.zeros_like(big)
+    big2[:, 3:10] = torch.from_numpy(np.array(list(zip(*states)), dtype=npdt)).cuda()
+    st.advance(big2[:, 3:10], 10)
+    np.testing.assert_array_equal(big2[:, 3:10].cpu().numpy().astype(np.uint64), S)
+    assert int(big2[:, :3].cpu().numpy().astype(np.uint64).sum()) == 0  # neighbours untouched
