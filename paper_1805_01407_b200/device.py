@@ -226,10 +226,14 @@ def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, e
     """Kernel K4: reduce T outputs of each substream in-kernel; returns the
     48-byte slp_checksum as a uint8 CUDA tensor (no host synchronisation)."""
     gid = native_id(spec)
-    ld = states.shape[1]
-    n = ld if nstreams is None else int(nstreams)
-    if states.dtype != _word_dtype(spec.kind.w) or not states.is_cuda or states.shape[0] != spec.kind.k:
-        raise ValueError("bad states tensor")
+    if states.dim() != 2 or states.dtype != _word_dtype(spec.kind.w) or not states.is_cuda \
+            or states.shape[0] != spec.kind.k or states.stride(1) != 1:
+        raise ValueError(f"states must be a CUDA ({spec.kind.k}, ld) {_word_dtype(spec.kind.w)} tensor "
+                         "with unit column stride")
+    ld = states.stride(0) if spec.kind.k > 1 else states.shape[1]
+    n = states.shape[1] if nstreams is None else int(nstreams)
+    if n < 0 or n > states.shape[1]:
+        raise ValueError("bad nstreams")
     dev = states.device
     ws = _workspace(gid, dev)
     if result is None:

@@ -447,3 +447,17 @@ def test_vecstepper_numpy_and_strided_states(name):
     st.advance(big2[:, 3:10], 10)
     np.testing.assert_array_equal(big2[:, 3:10].cpu().numpy().astype(np.uint64), S)
     assert int(big2[:, :3].cpu().numpy().astype(np.uint64).sum()) == 0  # neighbours untouched
+
+
+def test_fused_checksum_on_column_slice():
+    """K4 on a column slice of a wider state tensor (row pitch != n) equals the
+    checksum of the same substreams stored contiguously."""
+    spec = P.get_spec("xoshiro512plusplus")
+    sub = D.Substreams.from_seed(spec, 42, 300)
+    ref = sub.states[:, 100:250].clone()
+    c_ref = D.fused_checksum(spec, ref, 333)
+    view = sub.states[:, 100:250]
+    c_view = D.fused_checksum(spec, view, 333)
+    assert (c_view.sum, c_view.xor, c_view.mant) == (c_ref.sum, c_ref.xor, c_ref.mant)
+    assert torch.equal(view, ref)  # advanced in place, identically
+    assert torch.equal(sub.states[:, :100], D.Substreams.from_seed(spec, 42, 300).states[:, :100])
