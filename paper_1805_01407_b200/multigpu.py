@@ -6,7 +6,7 @@ The reference's only decomposition is "clone + jump to partition the orbit"
 substreams (jump 2^(n/2)) x ``T`` outputs; GPU g of G takes the blocks
 b == g (mod G), so the set of outputs -- and therefore the checksum -- does
 not depend on G.  The data path needs no collective; the per-GPU checksums
-are combined with ONE all_gather of a 40-byte record per rank (NCCL has no
+are combined with ONE all_gather of a 64-byte record per rank (NCCL has no
 XOR reduction, nccl.h:260-264) and folded in rank order on every rank, which
 makes the result exact and identical everywhere.
 """
