@@ -40,4 +40,12 @@ def __getattr__(name):
 
         _d = importlib.import_module(__name__ + ".device")
         return _d if name == "device" else getattr(_d, name)
+    # the reference re-exports these from hwd (__init__.py:36); HwdCounters and
+    # batch_size size the reference's packed host counters, which the exact
+    # GPU counters of kernel K6 do not need
+    if name in ("hwd", "HwdConfig", "HwdReport", "choose_ell"):
+        import importlib
+
+        _h = importlib.import_module(__name__ + ".hwd")
+        return _h if name == "hwd" else getattr(_h, name)
     raise AttributeError(name)
