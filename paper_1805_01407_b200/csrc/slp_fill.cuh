@@ -58,7 +58,7 @@ __host__ __device__ constexpr FillCfg fill_cfg_at(int i) {
   }
 }
 constexpr int kNumFillCfgs = 5;
-enum { FILL_KIND_NATIVE = 0, FILL_KIND_CONVERT = 1, FILL_KIND_CHECKSUM = 2 };
+enum { FILL_KIND_NATIVE = 0, FILL_KIND_CONVERT = 1, FILL_KIND_CHECKSUM = 2, FILL_KIND_SHORT = 3 };
 }  // namespace dev
 }  // namespace slp
 #include "slp_fill_tuning.h"  // fill_tune(generator id, kind) -> configuration index (measured)
@@ -68,6 +68,8 @@ namespace dev {
 // -DSLP_FILL_CFG=i forces configuration i for every kernel (tuning builds,
 // profiles/tune_fill.py)
 __host__ __device__ constexpr FillCfg fill_cfg(int id, int kind) {
+  // short rows (T below one tuned tile): 256-byte pieces, two buffers
+  if (kind == FILL_KIND_SHORT) return FillCfg{2, 2, 0, 32};
 #ifdef SLP_FILL_CFG
   return (void)id, (void)kind, fill_cfg_at(SLP_FILL_CFG);
 #else
@@ -151,14 +153,14 @@ __device__ __forceinline__ void reduce_checksum_block(uint64_t slo, uint64_t shi
   }
 }
 
-template <class G, int OK, int MODE, bool CSUM = false>
+template <class G, int OK, int MODE, bool CSUM = false, bool SHORT = false>
 __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __grid_constant__ CUtensorMap tmap) {
   using word = typename G::word;
   using Cv = Out<OK, word>;
   using bits = typename Cv::bits;
   constexpr int K = G::k;
   constexpr int ES = sizeof(bits);
-  using Shape = FillShape<G, fill_kind<OK, CSUM>()>;
+  using Shape = FillShape<G, SHORT ? (int)FILL_KIND_SHORT : fill_kind<OK, CSUM>()>;
   constexpr int kFillBufs = Shape::bufs, kSegs = Shape::segs, kTileBytes = Shape::tile_bytes;
   constexpr int CH = Shape::row_bytes / ES;                       // outputs per substream per tile
   constexpr int EPC = 16 / ES;                                    // elements per 16-byte chunk
@@ -438,8 +440,9 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
 
 // ---- host launchers ----------------------------------------------------------------
 
-template <class G, int OK, int MODE, bool CSUM = false>
+template <class G, int OK, int MODE, bool CSUM = false, bool SHORT = false>
 int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) {
+  using Shape = FillShape<G, SHORT ? (int)FILL_KIND_SHORT : fill_kind<OK, CSUM>()>;
   using bits = typename Out<OK, typename G::word>::bits;
   constexpr int ES = sizeof(bits);
   FillParams p = p0;
@@ -447,15 +450,15 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof tmap);
   if constexpr (MODE == FILL_TMA) {
-    int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, FillShape<G, fill_kind<OK, CSUM>()>::segs);
+    int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, Shape::segs);
     if (rc != SLP_OK) return rc;
   } else if constexpr (MODE == FILL_POS_TMA) {
     int rc = make_store_tmap_pm(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out,
-                                FillShape<G, fill_kind<OK, CSUM>()>::row_bytes / ES);
+                                Shape::row_bytes / ES);
     if (rc != SLP_OK) return rc;
   }
-  auto kern = k_fill<G, OK, MODE, CSUM>;
-  const int smem = MODE == FILL_POS ? 0 : FillShape<G, fill_kind<OK, CSUM>()>::smem;
+  auto kern = k_fill<G, OK, MODE, CSUM, SHORT>;
+  const int smem = MODE == FILL_POS ? 0 : Shape::smem;
   p.nunits = (p.nstreams + 31) / 32;
   const int dev = current_device();
   static std::atomic<int> per_sm[64];  // occupancy per device, computed once (benign race: same value)
@@ -527,19 +530,26 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
                      fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs * 128 / es)
                ? FILL_POS_TMA
                : FILL_POS;
-  else if (layout == SLP_STREAM_MAJOR)
-    mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out,
-                  fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs)
+  else if (layout != SLP_STREAM_MAJOR)
+    return SLP_ERR_INVALID;
+  // stream-major rows shorter than one tuned tile take the short shape
+  // (256-byte pieces): otherwise every output would go through the tail path
+  const int segs = fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs;
+  const bool short_rows = layout == SLP_STREAM_MAJOR && p.T < (uint64_t)segs * 128 / es;
+  if (layout == SLP_STREAM_MAJOR)
+    mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, short_rows ? fill_cfg(0, FILL_KIND_SHORT).segs : segs)
                ? FILL_TMA
                : FILL_STAGED;
-  else
-    return SLP_ERR_INVALID;
-#define SLP_FILL_CASE(OKV)                                                     \
-  if (ok == OKV) {                                                             \
-    if (mode == FILL_TMA) return launch_fill<G, OKV, FILL_TMA>(p, st);         \
-    if (mode == FILL_STAGED) return launch_fill<G, OKV, FILL_STAGED>(p, st);   \
-    if (mode == FILL_POS_TMA) return launch_fill<G, OKV, FILL_POS_TMA>(p, st); \
-    return launch_fill<G, OKV, FILL_POS>(p, st);                               \
+#define SLP_FILL_CASE(OKV)                                                                              \
+  if (ok == OKV) {                                                                                      \
+    if (mode == FILL_TMA)                                                                               \
+      return short_rows ? launch_fill<G, OKV, FILL_TMA, false, true>(p, st)                             \
+                        : launch_fill<G, OKV, FILL_TMA>(p, st);                                         \
+    if (mode == FILL_STAGED)                                                                            \
+      return short_rows ? launch_fill<G, OKV, FILL_STAGED, false, true>(p, st)                          \
+                        : launch_fill<G, OKV, FILL_STAGED>(p, st);                                      \
+    if (mode == FILL_POS_TMA) return launch_fill<G, OKV, FILL_POS_TMA>(p, st);                          \
+    return launch_fill<G, OKV, FILL_POS>(p, st);                                                        \
   }
   if constexpr (W == 64) {
     SLP_FILL_CASE(SLP_OUT_NATIVE)

@@ -89,3 +89,20 @@ def test_many_units_per_warp(name):
     _, c = D.fill_checksum(spec, sub.states, T)
     oc = O.checksum(want, w)
     assert (c.sum, c.xor, c.mant) == (oc["sum"], oc["xor"], oc["mant"])
+
+
+@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro1024plusplus", "xoshiro128plusplus",
+                                  "xoroshiro64star", "xorshift128plus"])
+@pytest.mark.parametrize("T", [31, 32, 33, 64, 100, 127])
+def test_short_rows_vs_oracle(name, T):
+    """Rows shorter than one tuned tile use the short (256-byte) tile shape."""
+    spec = P.get_spec(name)
+    w = spec.kind.w
+    flat = _flat(spec, 1000, T)
+    want, want_S = O.vec_outputs(name, flat, T)
+    want = want.astype(np.uint64 if w == 64 else np.uint32)
+    for kind in _kinds(w):
+        sub = D.Substreams.from_states(spec, flat)
+        got = sub.fill(T, kind=kind).cpu().numpy()
+        np.testing.assert_array_equal(_bits(got), _bits(_convert(want, kind, w)), err_msg=f"{name} {kind} T={T}")
+        np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
