@@ -11,5 +11,5 @@ python bench.py --steps 3 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_ou
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1.csv \
   python bench.py --steps 3 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu-launch rc=$?"
 python profiles/ncu_target.py > gpurun_out/target.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on --kernel-name-base function -k regex:'k_fill|k_fused$|k_jump' -s 2 -c 6 \
+  ncu --set full --clock-control none --import-source on --kernel-name-base function -k regex:'k_fill|k_fused$' -s 2 -c 2 \
   -o gpurun_out/prof_r1 python profiles/ncu_target.py > gpurun_out/ncu_full_r1.log 2>&1; echo "ncu-full rc=$?"
