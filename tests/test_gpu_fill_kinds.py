@@ -106,3 +106,22 @@ def test_short_rows_vs_oracle(name, T):
         got = sub.fill(T, kind=kind).cpu().numpy()
         np.testing.assert_array_equal(_bits(got), _bits(_convert(want, kind, w)), err_msg=f"{name} {kind} T={T}")
         np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
+
+
+@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro1024starstar", "xoshiro128plus"])
+@pytest.mark.parametrize("T", [1000, 1151, 300])
+def test_ragged_tail_without_state_write_back(name, T):
+    """Whole tiles + k_fill_tail, also when the caller does not advance the
+    states (the tile kernel then hands the tail its states in a temporary)."""
+    spec = P.get_spec(name)
+    w = spec.kind.w
+    flat = _flat(spec, 77, T)
+    want, want_S = O.vec_outputs(name, flat, T)
+    want = want.astype(np.uint64 if w == 64 else np.uint32)
+    sub = D.Substreams.from_states(spec, flat)
+    got = sub.fill(T, advance=False).cpu().numpy()
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), flat)  # untouched
+    got2 = sub.fill(T).cpu().numpy()
+    np.testing.assert_array_equal(got2, want)
+    np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
