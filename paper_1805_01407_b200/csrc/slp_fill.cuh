@@ -549,32 +549,49 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
   FillParams p = p0;
   if (grid_out) *grid_out = 0;
   if constexpr ((MODE == FILL_TMA || MODE == FILL_STAGED) && !CSUM) {
-    // whole tiles here, the rest in k_fill_tail (the tile kernel has no tail code)
+    // whole tiles here; of the rest, whole short tiles (256-byte rows) in the
+    // short-shape kernel and the last < 256 bytes per row in k_fill_tail
+    // (the tile kernels carry no tail code)
     constexpr uint64_t CH = Shape::row_bytes / ES;
+    constexpr uint64_t CHS = (uint64_t)fill_cfg(0, FILL_KIND_SHORT).segs * 128 / ES;
     const uint64_t rem = p.T % CH, Tm = p.T - rem;
+    const uint64_t Ts = SHORT ? 0 : rem - rem % CHS, rem2 = rem - Ts;
     if (rem != 0 && p.nstreams != 0) {
       void *tmp = nullptr;
       void *mid = p.sout;
+      if ((Tm > 0 || Ts > 0) && !mid) {  // no write-back requested: later parts still need the states
+        const size_t bytes = (size_t)G::k * p.ld * sizeof(typename G::word);
+        if (cudaMallocAsync(&tmp, bytes, st) != cudaSuccess) return cuda_fail("cudaMallocAsync(tail states)");
+        mid = tmp;
+      }
+      const void *src = p.sin;
+      int rc = SLP_OK;
       if (Tm > 0) {
-        if (!mid) {  // no write-back requested: the tail still needs the advanced states
-          const size_t bytes = (size_t)G::k * p.ld * sizeof(typename G::word);
-          if (cudaMallocAsync(&tmp, bytes, st) != cudaSuccess) return cuda_fail("cudaMallocAsync(tail states)");
-          mid = tmp;
-        }
         FillParams pm = p;
         pm.T = Tm;
         pm.sout = mid;
-        const int rc = launch_fill<G, OK, MODE, CSUM, SHORT>(pm, st, nullptr);
-        if (rc != SLP_OK) {
-          if (tmp) cudaFreeAsync(tmp, st);
-          return rc;
-        }
+        rc = launch_fill<G, OK, MODE, CSUM, SHORT>(pm, st, nullptr);
+        src = mid;
       }
-      FillParams pt = p;
-      pt.sin = Tm > 0 ? mid : p.sin;
-      pt.T = rem;
-      pt.out = static_cast<uint8_t *>(p.out) + Tm * ES;
-      const int rc = launch_fill_tail<G, OK>(pt, st);
+      if (rc == SLP_OK && Ts > 0) {
+        FillParams ps = p;
+        ps.sin = src;
+        ps.sout = mid;
+        ps.T = Ts;
+        ps.out = static_cast<uint8_t *>(p.out) + Tm * ES;
+        const bool tma = MODE == FILL_TMA &&
+                         tma_ok(ps.out, ES, Ts, p.nstreams, p.ld_out, fill_cfg(0, FILL_KIND_SHORT).segs);
+        rc = tma ? launch_fill<G, OK, FILL_TMA, false, true>(ps, st, nullptr)
+                 : launch_fill<G, OK, FILL_STAGED, false, true>(ps, st, nullptr);
+        src = mid;
+      }
+      if (rc == SLP_OK && rem2 > 0) {
+        FillParams pt = p;
+        pt.sin = src;
+        pt.T = rem2;
+        pt.out = static_cast<uint8_t *>(p.out) + (Tm + Ts) * ES;
+        rc = launch_fill_tail<G, OK>(pt, st);
+      }  // (rem2 == 0: the states already sit in mid, which is p.sout when requested)
       if (tmp) cudaFreeAsync(tmp, st);
       return rc;
     }
