@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
 
     for (uint64_t c = 0; c < ntiles; ++c) {
       const uint64_t pos0 = c * CH;
+      bits *const pos_row = out + pos0 * p.ld_out + stream;  // FILL_POS: row pos0, this lane's column
       uint32_t tile = 0;
       auto wait_buffer = [&] {
         if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA) {
@@ -276,9 +277,20 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       };
       auto emit = [&](uint32_t b, int e, const bits(&v)[EPC]) {
         if constexpr (MODE == FILL_POS) {
-          if (valid) {
+          // predicated stores (no branch per chunk): a branch per chunk let
+          // the compiler hoard a sub-block of outputs (255 registers + spills)
+          bits *ptr = pos_row + (uint64_t)(b + e) * p.ld_out;
 #pragma unroll
-            for (int i = 0; i < EPC; ++i) out[(pos0 + b + e + i) * p.ld_out + stream] = v[i];
+          for (int i = 0; i < EPC; ++i) {
+            bits *q = ptr + (uint64_t)i * p.ld_out;
+            if constexpr (ES == 8)
+              asm volatile("{\n\t.reg .pred pv;\n\tsetp.ne.u32 pv, %2, 0;\n\t@pv st.global.b64 [%0], %1;\n\t}" ::"l"(q),
+                           "l"((uint64_t)v[i]), "r"((uint32_t)valid)
+                           : "memory");
+            else
+              asm volatile("{\n\t.reg .pred pv;\n\tsetp.ne.u32 pv, %2, 0;\n\t@pv st.global.b32 [%0], %1;\n\t}" ::"l"(q),
+                           "r"((uint32_t)v[i]), "r"((uint32_t)valid)
+                           : "memory");
           }
         } else {
           put(b, e, v);
