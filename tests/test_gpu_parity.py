@@ -461,3 +461,17 @@ def test_fused_checksum_on_column_slice():
     assert (c_view.sum, c_view.xor, c_view.mant) == (c_ref.sum, c_ref.xor, c_ref.mant)
     assert torch.equal(view, ref)  # advanced in place, identically
     assert torch.equal(sub.states[:, :100], D.Substreams.from_seed(spec, 42, 300).states[:, :100])
+
+
+def test_host_chunks_sliced_staging(monkeypatch):
+    """A superbatch larger than the pinned staging slice is delivered through
+    several slices (bounded pinned memory), unchanged."""
+    monkeypatch.setattr(P.LanedStream, "_STAGE_VALUES", 1000)
+    spec = P.get_spec("xoroshiro128plusplus")
+    total = 3 * 64 * 500 + 123
+    host = list(P.LanedStream(spec, seed=4, lanes=64, lane_len=500).chunks(total))
+    want = O.laned_stream("xoroshiro128plusplus", 4, total, 64, 500)
+    np.testing.assert_array_equal(np.concatenate(host), want)
+    assert [h.size for h in host] == [32000, 32000, 32000, 123]
+    views = [v.copy() for v in P.LanedStream(spec, seed=4, lanes=64, lane_len=500).chunks(total, _views=True)]
+    np.testing.assert_array_equal(np.concatenate(views), want)
