@@ -1,0 +1,96 @@
+"""Seeded random sweep over the fill parameter space against the oracle:
+generator, substream count, row length (short rows, whole tiles, tails),
+layout, output kind, row pitch (padding) and an element offset of the output
+(alignment: TMA, staged and direct paths), with and without state
+write-back.  Every case is bit-exact or the test fails with its parameters."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1805_01407_b200 as P
+from paper_1805_01407_b200 import device as D
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ALL = P.registry_names(include_analysis=True)
+
+
+def _case(rng):
+    name = ALL[rng.integers(len(ALL))]
+    n = int(rng.choice([1, 31, 32, 33, 100, 257, 1000, 5000]))
+    T = int(rng.choice([1, 2, 15, 16, 31, 32, 33, 63, 64, 65, 100, 127, 128, 129, 255, 256, 300, 511, 512, 513,
+                        1000, 1024, 1151]))
+    layout = str(rng.choice(["stream", "position"]))
+    pad = int(rng.choice([0, 0, 0, 1, 3, 16]))
+    off = int(rng.choice([0, 0, 0, 1, 2]))
+    advance = bool(rng.integers(2))
+    return name, n, T, layout, pad, off, advance
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SLP_FUZZ_SEEDS", "12"))))
+def test_fill_fuzz(seed):
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(12):
+        name, n, T, layout, pad, off, advance = _case(rng)
+        spec = P.get_spec(name)
+        w = spec.kind.w
+        kinds = ["native", "f64"] if w == 64 else ["native", "u64", "f32"]
+        kind = kinds[rng.integers(len(kinds))]
+        flat = rng.integers(0, 1 << 63, size=(spec.kind.k, n), dtype=np.uint64) | np.uint64(1)
+        if w == 32:
+            flat &= np.uint64(0xFFFFFFFF)
+        want, want_S = O.vec_outputs(name, flat, T)
+        want = want.astype(np.uint64 if w == 64 else np.uint32)
+        if kind == "u64":
+            want = want.astype(np.uint64)
+        elif kind == "f64":
+            want = O.to_f64(want)
+        elif kind == "f32":
+            want = O.to_f32(want)
+        if layout == "position":
+            want = want.T.copy()
+        rows, cols = want.shape
+        dt = {np.dtype(np.uint64): torch.uint64, np.dtype(np.uint32): torch.uint32,
+              np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32}[want.dtype]
+        big = torch.zeros((rows, cols + pad + off), dtype=dt, device="cuda")
+        out = big[:, off:off + cols]
+        sub = D.Substreams.from_states(spec, flat)
+        D.fill(spec, sub.states, T, out=out, kind=kind, layout=layout, advance=advance)
+        got = out.cpu().numpy()
+        msg = f"{name} n={n} T={T} {layout} {kind} pad={pad} off={off} advance={advance}"
+        np.testing.assert_array_equal(got.view(np.uint8), want.view(np.uint8), err_msg=msg)
+        states = sub.states.cpu().numpy().astype(np.uint64)
+        np.testing.assert_array_equal(states, want_S if advance else flat, err_msg=msg)
+        if pad or off:  # nothing outside the output view is touched
+            rest = big.cpu().numpy().view(np.uint8).reshape(rows, -1)
+            es = big.element_size()
+            assert not rest[:, : off * es].any() and not rest[:, (off + cols) * es:].any(), msg
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SLP_FUZZ_SEEDS", "12"))))
+def test_checksum_fuzz(seed):
+    """Fused consumer (K4) and store + checksum (K2 CSUM) on random shapes."""
+    rng = np.random.default_rng(5000 + seed)
+    for _ in range(8):
+        name = ALL[rng.integers(len(ALL))]
+        spec = P.get_spec(name)
+        w = spec.kind.w
+        n = int(rng.choice([1, 32, 45, 300, 3000]))
+        T = int(rng.choice([1, 16, 17, 100, 128, 129, 512, 1000, 1024]))
+        flat = rng.integers(0, 1 << 63, size=(spec.kind.k, n), dtype=np.uint64) | np.uint64(1)
+        if w == 32:
+            flat &= np.uint64(0xFFFFFFFF)
+        want, want_S = O.vec_outputs(name, flat, T)
+        oc = O.checksum(want, w)
+        msg = f"{name} n={n} T={T}"
+        c = D.Substreams.from_states(spec, flat).checksum(T, exact=True, f64=bool(rng.integers(2)))
+        assert (c.sum, c.xor, c.mant) == (oc["sum"], oc["xor"], oc["mant"]), msg
+        sub = D.Substreams.from_states(spec, flat)
+        kind = "native" if rng.integers(2) else ("f64" if w == 64 else "f32")
+        out, c2 = D.fill_checksum(spec, sub.states, T, kind=kind)
+        assert (c2.sum, c2.xor, c2.mant) == (oc["sum"], oc["xor"], oc["mant"]), msg + " " + kind
+        np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S, err_msg=msg)
