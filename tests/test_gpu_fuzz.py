@@ -94,3 +94,28 @@ def test_checksum_fuzz(seed):
         out, c2 = D.fill_checksum(spec, sub.states, T, kind=kind)
         assert (c2.sum, c2.xor, c2.mant) == (oc["sum"], oc["xor"], oc["mant"]), msg + " " + kind
         np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S, err_msg=msg)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SLP_FUZZ_SEEDS", "12")) // 3 + 1))
+def test_init_fuzz(seed):
+    """Substream set-up (K1 + K1t) with random strides, block strides and
+    counts, sampled against host jumps (Generator.jump, generators.py:315-334)."""
+    rng = np.random.default_rng(9000 + seed)
+    for _ in range(3):
+        name = ALL[rng.integers(len(ALL))]
+        spec = P.get_spec(name)
+        nb = spec.kind.n
+        n = int(rng.choice([1, 7, 1000, 20000, 70000]))
+        blocks = int(rng.choice([1, 2, 3]))
+        stride = int(rng.integers(1, 1 << 62)) << int(rng.integers(0, nb // 2))
+        bstride = int(rng.integers(1, 1 << 62)) << int(rng.integers(0, nb // 2))
+        g0 = P.Generator.from_seed(spec, int(rng.integers(1 << 32)))
+        sub = D.Substreams.from_generator(g0, n, stride=stride, blocks=blocks, block_stride=bstride)
+        S = sub.states.cpu().numpy().astype(np.uint64)
+        for _ in range(4):
+            b, i = int(rng.integers(blocks)), int(rng.integers(n))
+            g = g0.clone()
+            steps = b * bstride + i * stride
+            if steps:
+                g.jump(P.compute_jump_poly(spec, steps))
+            assert list(g.flat_words()) == [int(v) for v in S[:, b * n + i]], (name, n, blocks, b, i)
