@@ -119,3 +119,32 @@ def test_init_fuzz(seed):
             if steps:
                 g.jump(P.compute_jump_poly(spec, steps))
             assert list(g.flat_words()) == [int(v) for v in S[:, b * n + i]], (name, n, blocks, b, i)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SLP_FUZZ_SEEDS", "12")) // 3 + 1))
+def test_hwd_counts_fuzz(seed):
+    """HWD counting (K6) on random ranges, k, modes and generators against the
+    oracle's per-signature counts and weight sums (hwd.py:206-233)."""
+    from paper_1805_01407_b200 import hwd
+
+    rng = np.random.default_rng(7000 + seed)
+    for _ in range(3):
+        split = bool(rng.integers(4) == 0)
+        names = [n for n in ALL if P.get_spec(n).kind.w == 64] if split else ALL
+        name = names[rng.integers(len(names))]
+        spec = P.get_spec(name)
+        w = 32 if split else spec.kind.w
+        k = int(rng.choice([1, 2, 3, 5, 8, 9, 10]))
+        mode = "transitional" if rng.integers(2) else "standard"
+        cfg = hwd.HwdConfig(w=w, k=k, mode=mode, split=split)
+        c0 = int(rng.integers(k, 5000))
+        c1 = c0 + int(rng.integers(1, 200_000))
+        seed_g = int(rng.integers(1 << 30))
+        ctr = hwd._GpuCounter(spec, seed_g, cfg)
+        ctr.count(c0, c1)
+        got_c, got_s = ctr.snapshot()
+        vals = O.hwd_test_values(name, seed_g, c1, split, mode == "transitional", w)
+        want_c, want_s = O.hwd_counts(vals, c0, c1, k, w, cfg.ell)
+        msg = f"{name} k={k} {mode} split={split} [{c0}, {c1})"
+        np.testing.assert_array_equal(got_c, want_c, err_msg=msg)
+        np.testing.assert_array_equal(got_s, want_s, err_msg=msg)
