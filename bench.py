@@ -180,9 +180,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SLP_BENCH_SHARE_GPU=1 (flow check of the N > 1 path on a one-GPU box, not a
+    # measurement): every rank uses cuda:0 and gloo carries the collectives
+    share = os.environ.get("SLP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     spec = P.get_spec(GEN)
     k = spec.kind.k
