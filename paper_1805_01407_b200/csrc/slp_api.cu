@@ -415,7 +415,7 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
     p.poly0 = l0.poly0;
     p.pmode = 2;
     p.use_base = 1;
-    p.count = l0.count;
+    p.count = l0.count < n ? l0.count : n;  // plans serve every n up to theirs (init_plan)
     p.m = 0;
     p.dst_off = 0;
     p.batch_stride = n;
@@ -424,7 +424,9 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
   }
   const DevTables *tabs = nullptr;
   for (size_t li = 1; li < plan->launches.size(); ++li) {
-    const InitLaunch &L = plan->launches[li];
+    InitLaunch L = plan->launches[li];
+    if (L.dst0 >= n) break;
+    if (L.count > n - L.dst0) L.count = n - L.dst0;
     if (L.uniform && use_jump_tables(L.count * nblocks)) {
       if (!tabs) {
         rc = plan_tables_on_device(*plan, id, dev, d_polys, st, &tabs);

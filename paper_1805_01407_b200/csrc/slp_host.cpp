@@ -563,10 +563,18 @@ const InitPlan &segment_plan(int id, const uint64_t *steps, int steps_words, uin
   return *res.first->second;
 }
 
-const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64_t n) {
+const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64_t n_req) {
   const int eid = engine_id(id);
   std::vector<uint64_t> st(steps, steps + steps_words);
   while (!st.empty() && st.back() == 0) st.pop_back();
+  // Plans are built for n = ndirect * 8^r >= n_req and serve every smaller
+  // count (the launches are a prefix; the caller clips them to its n), so a
+  // caller with many different counts (HWD ranges) shares O(log n) plans and
+  // their device tables instead of one per count.
+  const GenDesc &gd = *gen_desc(eid);
+  const uint64_t nd = gd.n() <= 256 ? kDirect : (gd.n() <= 512 ? kDirect / 4 : kDirect / 8);
+  uint64_t n = nd;
+  while (n < n_req) n *= kRadix;
   PlanKey key{eid, st, n};
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
