@@ -304,9 +304,17 @@ static int plan_tables_on_device(const InitPlan &plan, int id, int dev, const ui
   DevTables t;
   t.first_poly = plan.launches.size() > 1 ? plan.launches[1].poly0 : plan.polys.size() / plan.pw;
   t.count = plan.polys.size() / plan.pw - t.first_poly;
-  if (t.count > 0) {
+  // bounded: at most kMaxPlanTableSets table sets per device (a set is
+  // n^2/2 bytes per round polynomial: 0.7 MB for n = 256, 11 MB for
+  // n = 1024); further plans keep K1 for their rounds
+  static std::map<int, int> sets_per_dev;
+  constexpr int kMaxPlanTableSets = 64;
+  if (t.count > 0 && sets_per_dev[dev] < kMaxPlanTableSets) {
     const int rc = build_jump_tables(id, d_polys, t.first_poly, nullptr, t.count, st, &t.tables);
     if (rc != SLP_OK) return rc;
+    ++sets_per_dev[dev];
+  } else {
+    t.count = 0;
   }
   auto res = g_dev_tables.emplace(key, t);
   *out = &res.first->second;
@@ -432,6 +440,8 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
         rc = plan_tables_on_device(*plan, id, dev, d_polys, st, &tabs);
         if (rc != SLP_OK) return rc;
       }
+    }
+    if (L.uniform && tabs && tabs->tables && use_jump_tables(L.count * nblocks)) {
       TableJumpParams tp{};
       tp.src = states;
       tp.ld_src = ld;
