@@ -63,14 +63,11 @@ struct TableJumpParams {
 };
 
 // fill tile geometry (kernel K2): each warp emits tiles of 32 substreams x
-// segs x 128 bytes, one 3-D TMA store each, one CTA (7 warps) per SM.  Two
-// shapes, both 224 KiB of shared memory per CTA, chosen per generator
-// (FillShape in slp_device.cuh) by an A/B sweep over all 27
-// (profiles/round1_fill_geometry.md):
-//   narrow: 512-byte row pieces (segs 4) x 2 buffers per warp
-//   wide:   1 KiB row pieces (segs 8) x 1 buffer per warp
-// -DSLP_FILL_SEGS=.. -DSLP_FILL_BUFS=.. force one shape for every generator
-// (variant builds).
+// segs x 128 bytes, one TMA store each, one CTA of 7 warps per SM.  The tile
+// configuration (segs, buffers, pre-wait chunks, sub-block unroll) is chosen
+// per (generator, kind) from a measured table (FillCfg / fill_cfg in
+// slp_fill.cuh, slp_fill_tuning.h, profiles/tune_fill.py); -DSLP_FILL_CFG=i
+// forces one configuration for every kernel (A/B builds).
 #ifndef SLP_FILL_WARPS
 #define SLP_FILL_WARPS 7
 #endif
