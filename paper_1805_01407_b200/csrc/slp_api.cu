@@ -132,8 +132,8 @@ int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t ns
 }
 
 // Position-major output [T][ld_out] as a 2-D tensor (substream, position):
-// one box {32, ch} is ch positions x 32 consecutive substreams, no swizzle
-// (the shared tile is [position][lane]).
+// one box {box_rows, ch} is ch positions x box_rows consecutive substreams,
+// no swizzle (the shared tile is [position][substream]).
 bool tma_ok_pm(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int ch) {
   static int path = env_int("SLP_STORE_PATH", 0);
   if (path == 2) return false;
@@ -141,7 +141,8 @@ bool tma_ok_pm(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t 
          nstreams < (1ull << 31) && ld_out >= nstreams && ld_out * es < (1ull << 40) && ch <= 256;
 }
 
-int make_store_tmap_pm(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int ch) {
+int make_store_tmap_pm(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int ch,
+                       int box_rows) {
   auto fn = encode_fn();
   if (!fn) {
     set_last_error("cuTensorMapEncodeTiled unavailable");
@@ -149,7 +150,7 @@ int make_store_tmap_pm(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t
   }
   cuuint64_t gdim[2] = {(cuuint64_t)nstreams, (cuuint64_t)T};
   cuuint64_t gstride[1] = {(cuuint64_t)(ld_out * es)};
-  cuuint32_t box[2] = {32, (cuuint32_t)ch};
+  cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)ch};
   cuuint32_t estride[2] = {1, 1};
   CUresult r = fn(map, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, gdim, gstride,
                   box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

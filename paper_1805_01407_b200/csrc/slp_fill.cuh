@@ -455,6 +455,108 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
 
 // ---- host launchers ----------------------------------------------------------------
 
+// Position-major, 4-byte outputs (32-bit generators, native or f32): with one
+// substream per lane a warp's row piece is only 128 bytes (4.2 TB/s).  Here
+// each lane runs TWO substreams (row0 + lane and row0 + 32 + lane), so a
+// warp's tile is [64 positions][64 substreams] (256-byte rows) and leaves with
+// one 2-D TMA store of 64 x 64; two 16 KB buffers per warp.
+constexpr int kPm2Pos = 64;
+constexpr int kPm2TileBytes = kPm2Pos * 64 * 4;
+constexpr int kPm2Smem = kFillWarps * 2 * kPm2TileBytes + 1024;
+
+template <class G, int OK>
+__global__ void __launch_bounds__(kFillThreads) k_fill_pm2(FillParams p, const __grid_constant__ CUtensorMap tmap) {
+  using word = typename G::word;
+  using Cv = Out<OK, word>;
+  using bits = typename Cv::bits;
+  constexpr int K = G::k;
+  static_assert(sizeof(bits) == 4 && kPm2Pos % K == 0, "4-byte outputs, whole ring periods");
+  constexpr int MSK = G::best_mask(0, 0);
+  const int lane = threadIdx.x & 31;
+  const int warp = warp_uniform();
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t tiles = ((smem_u32(smem_raw) + 1023u) & ~1023u) + warp * 2 * kPm2TileBytes;
+  const word *__restrict__ sin = static_cast<const word *>(p.sin);
+  word *sout = static_cast<word *>(p.sout);
+  bits *__restrict__ out = static_cast<bits *>(p.out);
+  const uint64_t ntiles = p.T / kPm2Pos, rem = p.T - ntiles * kPm2Pos;
+  const uint64_t nunits = (p.nstreams + 63) / 64;
+  uint32_t issued = 0;
+  for (uint64_t u = (uint64_t)blockIdx.x * kFillWarps + warp; u < nunits; u += (uint64_t)gridDim.x * kFillWarps) {
+    const uint64_t row0 = u * 64;
+    const uint64_t stA = row0 + lane, stB = row0 + 32 + lane;
+    const bool vA = stA < p.nstreams, vB = stB < p.nstreams;
+    word a[K], b[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      a[j] = vA ? sin[j * p.ld + stA] : (word)0;
+      b[j] = vB ? sin[j * p.ld + stB] : (word)0;
+    }
+    for (uint64_t c = 0; c < ntiles; ++c) {
+      const uint32_t tile = tiles + (issued & 1) * kPm2TileBytes;
+      if (issued >= 2 && elect_one()) bulk_wait_read<1>();
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < kPm2Pos; ++t) {
+        const int o = t % K;
+        const bits xa = Cv::conv(G::template output_m<MSK>(a, o));
+        G::template step_m<MSK>(a, o);
+        const bits xb = Cv::conv(G::template output_m<MSK>(b, o));
+        G::template step_m<MSK>(b, o);
+        const uint32_t row = tile + t * 256 + lane * 4;
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(row), "r"((uint32_t)xa) : "memory");
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(row + 128), "r"((uint32_t)xb) : "memory");
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (elect_one()) {
+        tma_store_2d(&tmap, tile, (int)row0, (int)(c * kPm2Pos));
+        bulk_commit();
+      }
+      ++issued;
+    }
+    for (uint64_t t = 0; t < rem; ++t) {  // tail positions: coalesced warp rows
+      const bits xa = Cv::conv(G::next_flat(a));
+      const bits xb = Cv::conv(G::next_flat(b));
+      const uint64_t pos = ntiles * kPm2Pos + t;
+      if (vA) out[pos * p.ld_out + stA] = xa;
+      if (vB) out[pos * p.ld_out + stB] = xb;
+    }
+    if (sout) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (vA) sout[j * p.ld + stA] = a[j];
+        if (vB) sout[j * p.ld + stB] = b[j];
+      }
+    }
+  }
+  if (elect_one()) bulk_wait_all<0>();
+}
+
+template <class G, int OK>
+int launch_fill_pm2(const FillParams &p, cudaStream_t st) {
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof tmap);
+  int rc = make_store_tmap_pm(&tmap, p.out, 4, p.T, p.nstreams, p.ld_out, kPm2Pos, 64);
+  if (rc != SLP_OK) return rc;
+  auto kern = k_fill_pm2<G, OK>;
+  const int dev = current_device();
+  static std::atomic<int> attr_set[64];
+  if (dev < 0 || dev >= 64) return SLP_ERR_CUDA;
+  if (!attr_set[dev]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPm2Smem) != cudaSuccess)
+      return cuda_fail("cudaFuncSetAttribute(pm2)");
+    attr_set[dev] = 1;
+  }
+  const uint64_t nunits = (p.nstreams + 63) / 64;
+  if (nunits == 0 || p.T == 0) return SLP_OK;
+  const uint64_t want = (nunits + kFillWarps - 1) / kFillWarps;
+  const uint64_t cap = (uint64_t)sm_count(dev) * fill_grid_mult();
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  kern<<<grid, kFillThreads, kPm2Smem, st>>>(p, tmap);
+  return check_launch("k_fill_pm2");
+}
+
 template <class G, int OK, int MODE, bool CSUM = false, bool SHORT = false, bool TAIL = false>
 int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) {
   using Shape = FillShape<G, SHORT ? (int)FILL_KIND_SHORT : fill_kind<OK, CSUM>()>;
@@ -542,6 +644,13 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
   else
     return SLP_ERR_UNSUPPORTED;
   const int es = (ok == SLP_OUT_NATIVE) ? W / 8 : (ok == SLP_OUT_F32 ? 4 : 8);
+  if constexpr (W == 32) {
+    // position-major 4-byte outputs: two substreams per lane, 256-byte rows
+    if (layout == SLP_POSITION_MAJOR && es == 4 && tma_ok_pm(p.out, 4, p.T, p.nstreams, p.ld_out, kPm2Pos)) {
+      if (ok == SLP_OUT_F32) return launch_fill_pm2<G, SLP_OUT_F32>(p, st);
+      return launch_fill_pm2<G, SLP_OUT_NATIVE>(p, st);
+    }
+  }
   int mode;
   if (layout == SLP_POSITION_MAJOR)
     mode = tma_ok_pm(p.out, es, p.T, p.nstreams, p.ld_out,

@@ -122,6 +122,7 @@ int check_launch(const char *what);
 bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);
 int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);
 bool tma_ok_pm(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int ch);
-int make_store_tmap_pm(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int ch);
+int make_store_tmap_pm(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int ch,
+                       int box_rows = 32);
 
 }  // namespace slp
