@@ -38,7 +38,14 @@ def run(path, steps=300):
     return N * T * steps / (e0.elapsed_time(e1) / 1e3)
 
 
-libs = sys.argv[1:]
-for rep in range(3):
-    for p in libs:
-        print(p, "%.4g outputs/s" % run(p), flush=True)
+if __name__ == "__main__":
+    if sys.argv[1] == "--one":
+        print(sys.argv[2], "%.4g outputs/s" % run(sys.argv[2]), flush=True)
+    else:
+        import subprocess
+
+        # one process per library: two builds of the same kernels in one
+        # process can collide (their launches then fail with invalid argument)
+        for rep in range(3):
+            for p in sys.argv[1:]:
+                subprocess.run([sys.executable, __file__, "--one", p], check=True)
