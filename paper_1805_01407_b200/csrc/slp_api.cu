@@ -380,6 +380,60 @@ static bool state_ok(const GenDesc &g, const uint64_t *words) {
 
 extern "C" {
 
+// Radix rounds 1.. of an init plan over nblocks batches of n states
+// (batch b at states + b * n): stream m*c + s of a batch is stream s jumped
+// by x^(c*m*stride), K1t for the table-sized rounds, else K1.
+static int plan_rounds(const InitPlan &plan, int id, const GenOps *ops, int dev, const uint64_t *d_polys,
+                       void *states, uint64_t ld, uint64_t n, uint64_t nblocks, cudaStream_t st) {
+  int rc = SLP_OK;
+  const DevTables *tabs = nullptr;
+  for (size_t li = 1; li < plan.launches.size(); ++li) {
+    InitLaunch L = plan.launches[li];
+    if (L.dst0 >= n) break;
+    if (L.count > n - L.dst0) L.count = n - L.dst0;
+    if (L.uniform && use_jump_tables(L.count * nblocks)) {
+      if (!tabs) {
+        rc = plan_tables_on_device(plan, id, dev, d_polys, st, &tabs);
+        if (rc != SLP_OK) return rc;
+      }
+    }
+    if (L.uniform && tabs && tabs->tables && use_jump_tables(L.count * nblocks)) {
+      TableJumpParams tp{};
+      tp.src = states;
+      tp.ld_src = ld;
+      tp.dst = states;
+      tp.ld_dst = ld;
+      tp.tables = tabs->tables;
+      tp.table0 = L.poly0 - tabs->first_poly;
+      tp.count = L.count;
+      tp.m = L.m;
+      tp.src_off = 0;
+      tp.dst_off = L.dst0;
+      tp.batch_stride = n;
+      rc = ops->jump_table(tp, nblocks, st);
+      if (rc != SLP_OK) return rc;
+      continue;
+    }
+    JumpParams p{};
+    p.src = states;
+    p.ld_src = ld;
+    p.dst = states;
+    p.ld_dst = ld;
+    p.polys = d_polys;
+    p.poly0 = L.poly0;
+    p.pmode = 1;
+    p.use_base = 0;
+    p.count = L.count;
+    p.m = L.m;
+    p.src_off = 0;
+    p.dst_off = L.dst0;
+    p.batch_stride = n;
+    rc = ops->jump(p, nullptr, L.uniform, nblocks, st);
+    if (rc != SLP_OK) return rc;
+  }
+  return SLP_OK;
+}
+
 int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, const uint64_t *steps, int steps_words,
                         void *states, uint64_t ld, uint64_t n, void *stream) {
   const GenDesc *g = gen_desc(id);
@@ -431,52 +485,7 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
     rc = ops->jump(p, &base, false, nb, st);
     if (rc != SLP_OK) return rc;
   }
-  const DevTables *tabs = nullptr;
-  for (size_t li = 1; li < plan->launches.size(); ++li) {
-    InitLaunch L = plan->launches[li];
-    if (L.dst0 >= n) break;
-    if (L.count > n - L.dst0) L.count = n - L.dst0;
-    if (L.uniform && use_jump_tables(L.count * nblocks)) {
-      if (!tabs) {
-        rc = plan_tables_on_device(*plan, id, dev, d_polys, st, &tabs);
-        if (rc != SLP_OK) return rc;
-      }
-    }
-    if (L.uniform && tabs && tabs->tables && use_jump_tables(L.count * nblocks)) {
-      TableJumpParams tp{};
-      tp.src = states;
-      tp.ld_src = ld;
-      tp.dst = states;
-      tp.ld_dst = ld;
-      tp.tables = tabs->tables;
-      tp.table0 = L.poly0 - tabs->first_poly;
-      tp.count = L.count;
-      tp.m = L.m;
-      tp.src_off = 0;
-      tp.dst_off = L.dst0;
-      tp.batch_stride = n;
-      rc = ops->jump_table(tp, nblocks, st);
-      if (rc != SLP_OK) return rc;
-      continue;
-    }
-    JumpParams p{};
-    p.src = states;
-    p.ld_src = ld;
-    p.dst = states;
-    p.ld_dst = ld;
-    p.polys = d_polys;
-    p.poly0 = L.poly0;
-    p.pmode = 1;
-    p.use_base = 0;
-    p.count = L.count;
-    p.m = L.m;
-    p.src_off = 0;
-    p.dst_off = L.dst0;
-    p.batch_stride = n;
-    rc = ops->jump(p, nullptr, L.uniform, nblocks, st);
-    if (rc != SLP_OK) return rc;
-  }
-  return SLP_OK;
+  return plan_rounds(*plan, id, ops, dev, d_polys, states, ld, n, nblocks, st);
 }
 
 int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, const uint64_t *seg_steps,
@@ -491,7 +500,7 @@ int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, co
     return SLP_ERR_INVALID;
   const InitPlan *plan;
   try {
-    plan = &segment_plan(id, seg_steps, seg_words, J);
+    plan = &init_plan(id, seg_steps, seg_words, J);  // segment j = substream jumped by x^(j*seg)
   } catch (const AlgebraError &e) {
     set_last_error(e.what());
     return SLP_ERR_ALGEBRA;
@@ -504,19 +513,39 @@ int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, co
   const uint64_t *d_polys = nullptr;
   int rc = plan_polys_on_device(*plan, dev, &d_polys);
   if (rc != SLP_OK) return rc;
-  JumpParams p{};
-  p.src = states;
-  p.ld_src = ld;
-  p.dst = seg_states;
-  p.ld_dst = ld_seg;
-  p.polys = d_polys;
-  p.poly0 = 0;
-  p.pmode = 3;  // segment (i, j) = state i jumped by x^(j*seg), i-major
-  p.use_base = 0;
-  p.count = n * J;
-  p.m = J;
-  p.batch_stride = 0;
-  return ops->jump(p, nullptr, false, 1, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t esize = g->w / 8;
+  // the init plan with the n substreams as its batches: launch 0 jumps each
+  // substream directly into its first segments, the radix rounds grow the rest
+  const InitLaunch &l0 = plan->launches[0];
+  for (uint64_t b0 = 0; b0 < n; b0 += 65535) {
+    const uint64_t nb = n - b0 < 65535 ? n - b0 : 65535;
+    void *seg = static_cast<uint8_t *>(seg_states) + b0 * J * esize;
+    JumpParams p{};
+    p.src = static_cast<const uint8_t *>(states) + b0 * esize;
+    p.ld_src = ld;
+    p.dst = seg;
+    p.ld_dst = ld_seg;
+    p.polys = d_polys;
+    p.poly0 = l0.poly0;
+    p.pmode = 2;
+    p.use_base = 0;
+    p.count = l0.count < J ? l0.count : J;
+    p.m = 1;  // source = the batch's own substream
+    p.batch_stride = J;
+    p.src_batch_stride = 1;
+    uint64_t grid_batches = nb;
+    if (p.count < 128) {  // fewer states than a CTA per substream: fold the substreams into x
+      p.fold = p.count;
+      p.count *= nb;
+      grid_batches = 1;
+    }
+    rc = ops->jump(p, nullptr, false, grid_batches, st);
+    if (rc != SLP_OK) return rc;
+    rc = plan_rounds(*plan, id, ops, dev, d_polys, seg, ld_seg, J, nb, st);
+    if (rc != SLP_OK) return rc;
+  }
+  return SLP_OK;
 }
 
 int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *src, uint64_t ld_src, void *dst,

@@ -534,35 +534,6 @@ struct PlanKey {
 static std::mutex g_plan_mu;
 static std::map<PlanKey, std::unique_ptr<InitPlan>> g_plans;
 
-// Polynomials x^(j*steps) mod P for j < J (segment split of long substreams);
-// cached like the init plans, with no launches.
-const InitPlan &segment_plan(int id, const uint64_t *steps, int steps_words, uint64_t J) {
-  const int eid = engine_id(id);
-  std::vector<uint64_t> st(steps, steps + steps_words);
-  while (!st.empty() && st.back() == 0) st.pop_back();
-  PlanKey key{eid, st, J | (1ull << 63)};
-  {
-    std::lock_guard<std::mutex> lk(g_plan_mu);
-    auto it = g_plans.find(key);
-    if (it != g_plans.end()) return *it->second;
-  }
-  const GenDesc &g = *gen_desc(eid);
-  const Poly &P = engine_char_poly(eid);
-  const Reducer red(P);
-  auto plan = std::make_unique<InitPlan>();
-  const int pw = (g.n() + 63) / 64;
-  plan->pw = pw;
-  const Poly xs = poly_x_pow(st.data(), (int)st.size(), P);
-  Poly cur = poly_mod(Poly{1}, P);
-  for (uint64_t j = 0; j < J; ++j) {
-    for (int i = 0; i < pw; ++i) plan->polys.push_back(i < (int)cur.size() ? cur[i] : 0);
-    cur = red.mulmod(cur, xs);
-  }
-  std::lock_guard<std::mutex> lk(g_plan_mu);
-  auto res = g_plans.emplace(std::move(key), std::move(plan));
-  return *res.first->second;
-}
-
 const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64_t n_req) {
   const int eid = engine_id(id);
   std::vector<uint64_t> st(steps, steps + steps_words);

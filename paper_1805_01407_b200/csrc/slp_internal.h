@@ -73,8 +73,6 @@ struct InitPlan {
   int device = -1;
 };
 const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64_t n);
-// x^(j*steps) mod P for j < J (polys only; segment split of long substreams)
-const InitPlan &segment_plan(int id, const uint64_t *steps, int steps_words, uint64_t J);
 
 void set_last_error(const std::string &s);
 

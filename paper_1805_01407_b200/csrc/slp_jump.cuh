@@ -19,42 +19,55 @@ template <class G, bool UNIFORM>
 __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __grid_constant__ BaseStates base) {
   using word = typename G::word;
   constexpr int K = G::k;
-  const uint64_t t = (uint64_t)blockIdx.x * kJumpThreads + threadIdx.x;
+  uint64_t t = (uint64_t)blockIdx.x * kJumpThreads + threadIdx.x;
   if (t >= p.count) return;
-  const uint64_t b = blockIdx.y;
+  uint64_t b = blockIdx.y;
+  if (p.fold) {  // few states per batch: fold the batches into x so the warps are full
+    b = t / p.fold;
+    t -= b * p.fold;
+  }
   word cur[K], acc[K];
   if (p.use_base) {
 #pragma unroll
     for (int j = 0; j < K; ++j) cur[j] = (word)base.w[b * K + j];
   } else {
     const word *src = static_cast<const word *>(p.src);
-    const uint64_t si = b * p.batch_stride + p.src_off + (p.pmode == 3 ? t / p.m : (p.m ? t % p.m : t));
+    const uint64_t sbs = p.src_batch_stride ? p.src_batch_stride : p.batch_stride;
+    const uint64_t si = b * sbs + p.src_off + (p.m ? t % p.m : t);
 #pragma unroll
     for (int j = 0; j < K; ++j) cur[j] = src[j * p.ld_src + si];
   }
 #pragma unroll
   for (int j = 0; j < K; ++j) acc[j] = 0;
   const uint64_t pidx =
-      p.poly0 + (p.pmode == 1 ? t / p.m : (p.pmode == 2 ? t : (p.pmode == 3 ? t % p.m : 0)));
+      p.poly0 + (p.pmode == 1 ? t / p.m : (p.pmode == 2 ? t : 0));
   const uint64_t *poly = p.polys ? p.polys + pidx * G::pw : base.w;  // slp_jump_states: poly in params
   const int pw_used = p.pw_used > 0 && p.pw_used < G::pw ? p.pw_used : G::pw;
+  // bits per unrolled chunk: the whole word for small states; 16 for k >= 8,
+  // whose 64-bit body (~27-61 KB of SASS) thrashes the instruction cache when
+  // few warps run (segment split, direct launches).  16 is a multiple of the
+  // ring length, so the register rotation stays static.
+  constexpr int UB = K >= 8 ? 16 : 64;
 #pragma unroll 1
   for (int wi = 0; wi < pw_used; ++wi) {
-    const uint64_t cb = poly[wi];
+    uint64_t cb = poly[wi];
+#pragma unroll 1
+    for (int c = 0; c < 64; c += UB, cb >>= (UB & 63)) {
 #pragma unroll
-    for (int bb = 0; bb < 64; ++bb) {
-      const int o = bb % K;
-      if constexpr (UNIFORM) {
-        if ((cb >> bb) & 1ull) {
+      for (int bb = 0; bb < UB; ++bb) {
+        const int o = bb % K;
+        if constexpr (UNIFORM) {
+          if ((cb >> bb) & 1ull) {
 #pragma unroll
-          for (int j = 0; j < K; ++j) acc[j] ^= cur[G::slot(o, j)];
+            for (int j = 0; j < K; ++j) acc[j] ^= cur[G::slot(o, j)];
+          }
+        } else {
+          const word msk = (word)0 - (word)((cb >> bb) & 1ull);
+#pragma unroll
+          for (int j = 0; j < K; ++j) acc[j] ^= cur[G::slot(o, j)] & msk;
         }
-      } else {
-        const word msk = (word)0 - (word)((cb >> bb) & 1ull);
-#pragma unroll
-        for (int j = 0; j < K; ++j) acc[j] ^= cur[G::slot(o, j)] & msk;
+        G::step(cur, o);
       }
-      G::step(cur, o);
     }
   }
   word *dst = static_cast<word *>(p.dst);

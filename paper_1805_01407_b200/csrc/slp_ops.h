@@ -40,12 +40,13 @@ struct JumpParams {
   uint64_t ld_dst;
   const uint64_t *polys;  // device, G::pw words per polynomial
   uint64_t poly0;
-  int pmode;              // 0: poly0 for all, 1: poly0 + t / m, 2: poly0 + t,
-                          // 3: source t / m with poly0 + t % m (segment split)
+  int pmode;              // 0: poly0 for all, 1: poly0 + t / m, 2: poly0 + t
   int use_base;           // source state = BaseStates entry of the batch
   uint64_t count;         // states per batch
   uint64_t m;             // source index t % m (0: t)
   uint64_t src_off, dst_off, batch_stride;
+  uint64_t src_batch_stride;  // source states per batch (0: batch_stride)
+  uint64_t fold;              // > 0: batches folded into t (batch t / fold, index t % fold), grid.y = 1
   int pw_used;            // polynomial words actually used (0 = all); trims the loop for low-degree polys
 };
 

@@ -166,16 +166,21 @@ def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor
     return out
 
 
-SPLIT_TARGET_THREADS = 1 << 17
+# the fill needs >= 2^18 substreams to reach its store rate; segments of
+# >= 2048 outputs and >= 8 per state bit amortise their jumps (profiles/
+# round1_split.jsonl)
+SPLIT_TARGET_THREADS = 1 << 18
+SPLIT_MIN_SEG = 2048
+SPLIT_SEG_PER_BIT = 8
 
 
 def _split_factor(spec: GeneratorSpec, n: int, T: int, layout: str, ld_out: int) -> int:
     """Segments per substream so that few, long substreams still fill the GPU.
     Only for contiguous stream-major output; each segment must be long enough
-    (64 x state bits outputs) to amortise its jump."""
+    to amortise its jump."""
     if layout != "stream" or ld_out != T or n == 0 or n >= SPLIT_TARGET_THREADS // 2:
         return 1
-    min_seg = max(4096, 64 * spec.kind.n)
+    min_seg = max(SPLIT_MIN_SEG, SPLIT_SEG_PER_BIT * spec.kind.n)
     J = 1
     while n * J < SPLIT_TARGET_THREADS and T % (2 * J) == 0 and T // (2 * J) >= min_seg:
         J *= 2

@@ -364,6 +364,37 @@ def test_segment_split_fill_is_transparent(name, n, T):
     assert torch.equal(a.states, ref.states)
 
 
+@pytest.mark.parametrize("name,n,J", [("xoshiro256starstar", 1, 1 << 14), ("xoroshiro128plus", 3, 3000),
+                                      ("xoshiro128plusplus", 40, 1500), ("xoroshiro1024starstar", 2, 1 << 12),
+                                      ("xoshiro512plus", 5, 7), ("xoroshiro64star", 70000, 2)])
+def test_split_substreams_segment_states(name, n, J):
+    """slp_split_substreams: segment j of substream i is substream i jumped by
+    j * seg steps (direct launch, radix rounds with K1 / K1t, batches of
+    65535 substreams), sampled against host jumps (generators.py:315-334)."""
+    import ctypes
+
+    from paper_1805_01407_b200 import _native
+
+    spec = P.get_spec(name)
+    rng = np.random.default_rng(n * 7 + J)
+    seg_len = int(rng.integers(1, 1 << 62)) << 3
+    sub = D.Substreams.from_seed(spec, 21, n, stride=1 << 40)
+    seg = torch.empty((spec.kind.k, n * J), dtype=sub.states.dtype, device="cuda")
+    sw, sn = _native.int_to_words(seg_len)
+    rc = _native.lib().slp_split_substreams(D.native_id(spec), ctypes.c_void_p(sub.states.data_ptr()), n, n, sw, sn,
+                                            J, ctypes.c_void_p(seg.data_ptr()), n * J, None)
+    assert rc == 0
+    S = sub.states.cpu().numpy().astype(np.uint64)
+    G = seg.cpu().numpy().astype(np.uint64)
+    picks = {(0, 0), (n - 1, J - 1)} | {(int(rng.integers(n)), int(rng.integers(J))) for _ in range(12)}
+    for i, j in sorted(picks):
+        g = P.Generator.from_seed(spec, 1)
+        g.set_flat_words(S[:, i])
+        if j:
+            g.jump(P.compute_jump_poly(spec, j * seg_len))
+        assert list(g.flat_words()) == [int(v) for v in G[:, i * J + j]], (name, i, j)
+
+
 def test_host_chunks_are_fresh_and_match_device_chunks():
     """Pipelined host delivery (staging double buffer + threaded copies) yields
     caller-owned arrays equal to the device chunks (generators.py:482)."""
