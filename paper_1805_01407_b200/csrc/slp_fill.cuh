@@ -206,8 +206,13 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
     for (int j = 0; j < K; ++j) s[j] = nxt[j];
     load_states(u + ustride, nxt);
 
-    for (uint64_t c = 0; c < ntiles; ++c) {
+    // TAIL: a ragged row's last rem < CH outputs form one more tile; its
+    // whole sub-blocks run through the same (rolled) code as a full tile
+    const uint64_t nloop = ntiles + (TAIL && rem >= (uint64_t)U ? 1 : 0);
+    uint32_t tail_tile = 0;
+    for (uint64_t c = 0; c < nloop; ++c) {
       const uint64_t pos0 = c * CH;
+      const uint32_t sub_end = (!TAIL || c < ntiles) ? (uint32_t)CH : (uint32_t)(rem / U) * U;
       bits *const pos_row = out + pos0 * p.ld_out + stream;  // FILL_POS: row pos0, this lane's column
       uint32_t tile = 0;
       auto wait_buffer = [&] {
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       // instruction cache (a fully unrolled 1 KiB-row tile of an 8-word
       // generator is ~60 KB of SASS, twice the 32 KB L1.5 I-cache)
 #pragma unroll 1
-      for (uint32_t b = U; b < (uint32_t)CH; b += U) {
+      for (uint32_t b = U; b < sub_end; b += U) {
 #pragma unroll
         for (int e = 0; e < U; e += EPC) {
           bits v[EPC];
@@ -337,6 +342,12 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
         cs_hi += t_hi >> 32;
         cs_x ^= (uint64_t)t_x;
         cs_low += t_low;
+      }
+      if constexpr (TAIL) {
+        if (c == ntiles) {  // the tail tile: completed and stored below
+          tail_tile = tile;
+          break;
+        }
       }
       if constexpr (MODE == FILL_TMA) {
         fence_proxy_async_smem();
@@ -354,17 +365,31 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
           bulk_commit();
         }
         ++issued;
+
       } else if constexpr (MODE == FILL_STAGED) {
         __syncwarp();
-        // element stores; CPR lanes cover one 128-byte segment of a row
+        // element stores.  8-byte outputs go row by row: each warp store is
+        // 32 consecutive outputs (256 B) of one row, 3.2 -> 4.7 TB/s for u64
+        // against segment-major order.  4-byte outputs keep segment-major
+        // order (one 128-byte segment of a row per store), which measured
+        // faster for them (2.46 vs 2.20 TB/s, profiles/ragged_bench.py).
         constexpr int CPR = 128 / ES;  // elements per segment
-        constexpr int RPP = 32 / CPR;  // rows per pass (1 for u32, 2 for u64)
+        constexpr int RL = kSegs * CPR;  // outputs per row in the tile
 #pragma unroll 4
-        for (int r0 = 0; r0 < 32 * kSegs; r0 += RPP) {
-          const int rs = r0 + lane / CPR;  // (seg, row) flattened seg-major
-          const int seg = rs / 32, r = rs % 32;
-          const int e = lane % CPR;
-          const uint64_t srow = row0 + r;
+        for (int f0 = 0; f0 < 32 * RL; f0 += 32) {
+          int r, seg, e;
+          if constexpr (ES == 8) {
+            const int f = f0 + lane;  // (row, column) flattened row-major
+            r = f / RL;
+            seg = (f % RL) / CPR;
+            e = f % CPR;
+          } else {
+            const int rs = f0 / CPR;  // (segment, row) flattened segment-major, CPR = 32
+            seg = rs / 32;
+            r = rs % 32;
+            e = lane;
+          }
+          const uint64_t grow = row0 + r;
           bits v;
           const uint32_t addr = tile + swz(seg, r, (e * ES) >> 4) + (e * ES & 15);
           if constexpr (ES == 8) {
@@ -372,7 +397,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
           } else {
             asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
           }
-          if (srow < p.nstreams) out[srow * p.ld_out + pos0 + seg * CPR + e] = v;
+          if (grow < p.nstreams) out[grow * p.ld_out + pos0 + seg * CPR + e] = v;
         }
         __syncwarp();
         ++issued;
@@ -390,13 +415,73 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
         }
         if (valid) out[(ntiles * CH + t) * p.ld_out + stream] = x;
       }
-    } else if constexpr (CSUM || TAIL) {
+    } else if constexpr (TAIL) {
+      if (rem > 0) {
+        // the tail tile: whole sub-blocks came from the loop above; the last
+        // rem % U outputs are generated one at a time into the same tile.  Its
+        // whole 128-byte pieces leave with the TMA store (the tensor map ends
+        // at the last whole piece of a row and clips the box); the final
+        // partial piece leaves with element stores.
+        const uint32_t rb = rem >= (uint64_t)U ? (uint32_t)(rem / U) * U : 0u;
+        uint32_t tile = tail_tile;
+        if (rb == 0) {
+          tile = tiles + (issued % kFillBufs) * kTileBytes;
+          if constexpr (MODE == FILL_TMA) {
+            if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
+          }
+          __syncwarp();
+        }
+        for (uint32_t t = rb; t < (uint32_t)rem; ++t) {
+          const bits x = Cv::conv(G::next_flat(s));
+          const uint32_t byte = t * ES;
+          const uint32_t addr = tile + swz(byte >> 7, lane, (byte & 127) >> 4) + (byte & 15);
+          if constexpr (ES == 8)
+            asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"((uint64_t)x) : "memory");
+          else
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"((uint32_t)x) : "memory");
+        }
+        constexpr int CPR = 128 / ES;  // elements per 128-byte piece
+        constexpr int RPP = 32 / CPR;  // rows per pass
+        int seg0 = 0;
+        if constexpr (MODE == FILL_TMA) {
+          seg0 = (int)(rem / CPR);
+          if (seg0 > 0) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (elect_one()) {
+              tma_store_3d(&tmap, tile, 0, (int)row0, (int)(ntiles * CH * ES / 128));
+              bulk_commit();
+            }
+            ++issued;  // only a committed store owns its buffer (bulk_wait_read counts groups)
+          }
+        }
+        __syncwarp();
+        const int nseg = (int)((rem + CPR - 1) / CPR);
+        for (int r0 = 32 * seg0; r0 < 32 * nseg; r0 += RPP) {
+          const int rs = r0 + lane / CPR;  // (piece, row) flattened piece-major
+          const int seg = rs / 32, r = rs % 32;
+          const int e = lane % CPR;
+          const uint64_t col = (uint64_t)seg * CPR + e;
+          const uint64_t grow = row0 + r;
+          if (col < rem && grow < p.nstreams) {
+            bits v;
+            const uint32_t addr = tile + swz(seg, r, (e * ES) >> 4) + (e * ES & 15);
+            if constexpr (ES == 8) {
+              asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+            } else {
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+            }
+            out[grow * p.ld_out + ntiles * CH + col] = v;
+          }
+        }
+        __syncwarp();
+      }
+    } else if constexpr (CSUM) {
       if (rem > 0) {
       // stream-major tail (T not a multiple of the tile): the last rem < CH
       // outputs of each row go through the warp's tile right after its last
-      // tile and leave with coalesced element stores.  Only the TAIL (and
-      // CSUM) instances carry this code: in the tail-free instance used for
-      // whole tiles it doubled the registers (48 -> 102) and cost 2%.
+      // tile and leave with coalesced element stores (the store + checksum
+      // instance; the fill's TAIL instance above reuses the tile loop).
       const uint32_t tile = tiles + (issued % kFillBufs) * kTileBytes;
       if constexpr (MODE == FILL_TMA) {
         if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
@@ -426,8 +511,8 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
         const int seg = rs / 32, r = rs % 32;
         const int e = lane % CPR;
         const uint64_t col = (uint64_t)seg * CPR + e;
-        const uint64_t srow = row0 + r;
-        if (col < rem && srow < p.nstreams) {
+        const uint64_t grow = row0 + r;
+        if (col < rem && grow < p.nstreams) {
           bits v;
           const uint32_t addr = tile + swz(seg, r, (e * ES) >> 4) + (e * ES & 15);
           if constexpr (ES == 8) {
@@ -435,7 +520,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
           } else {
             asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
           }
-          out[srow * p.ld_out + ntiles * CH + col] = v;
+          out[grow * p.ld_out + ntiles * CH + col] = v;
         }
       }
       __syncwarp();
@@ -663,10 +748,10 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
   // (256-byte pieces): otherwise every output would go through the tail path
   const int segs = fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs;
   const bool short_rows = layout == SLP_STREAM_MAJOR && p.T < (uint64_t)segs * 128 / es;
-  if (layout == SLP_STREAM_MAJOR)
-    mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, short_rows ? fill_cfg(0, FILL_KIND_SHORT).segs : segs)
-               ? FILL_TMA
-               : FILL_STAGED;
+  if (layout == SLP_STREAM_MAJOR) {
+    const int ssegs = short_rows ? fill_cfg(0, FILL_KIND_SHORT).segs : segs;
+    mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, ssegs) ? FILL_TMA : FILL_STAGED;
+  }
 #define SLP_FILL_CASE(OKV)                                                                              \
   if (ok == OKV) {                                                                                      \
     if (mode == FILL_TMA)                                                                               \

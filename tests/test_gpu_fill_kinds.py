@@ -125,3 +125,36 @@ def test_ragged_tail_without_state_write_back(name, T):
     got2 = sub.fill(T).cpu().numpy()
     np.testing.assert_array_equal(got2, want)
     np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
+
+
+@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro128plusplus", "xoroshiro1024star",
+                                  "xoshiro128starstar", "xoroshiro64starstar"])
+@pytest.mark.parametrize("T,n,pad", [(1055, 1001, 0), (127, 37, 0), (2047, 70, 0), (1026, 33, 0), (1024, 65, 1),
+                                     (300, 64, 3), (1151, 3, 0)])
+def test_odd_pitch_rows(name, T, n, pad):
+    """Stream-major rows whose pitch is not a multiple of 16 bytes (TMA needs
+    16-byte aligned row starts, profiles/tma_align_probe.cu) take the staged
+    path; tails and short rows included.  Bytes after the last row and in
+    the row padding stay untouched."""
+    import torch
+
+    spec = P.get_spec(name)
+    w = spec.kind.w
+    flat = _flat(spec, n, T + n)
+    want_i, want_S = O.vec_outputs(name, flat, T)
+    for kind in _kinds(w):
+        want = _convert(want_i.astype(np.uint64 if w == 64 else np.uint32), kind, w)
+        dt = {np.dtype(np.uint64): torch.uint64, np.dtype(np.uint32): torch.uint32,
+              np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32}[want.dtype]
+        ld = T + pad
+        flatbuf = torch.zeros(n * ld + 64, dtype=dt, device="cuda")
+        out = flatbuf[: n * ld].view(n, ld)[:, :T]
+        sub = D.Substreams.from_states(spec, flat)
+        D.fill(spec, sub.states, T, out=out, kind=kind)
+        got = out.cpu().numpy()
+        np.testing.assert_array_equal(got.view(np.uint8), want.view(np.uint8), err_msg=f"{name} {kind}")
+        np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S)
+        rest = flatbuf.cpu().numpy()
+        assert not rest[n * ld:].view(np.uint8).any()
+        if pad:
+            assert not rest[: n * ld].reshape(n, ld)[:, T:].view(np.uint8).any()
