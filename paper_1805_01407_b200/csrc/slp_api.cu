@@ -162,6 +162,63 @@ int make_store_tmap_pm(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t
   return SLP_OK;
 }
 
+// Row alignment of the tile pieces: a 32-byte sector for 8-byte outputs
+// (odd T: 4.2-4.9 TB/s against 3.8-4.3 with 16-byte alignment); 16 bytes for
+// 4-byte outputs, where sector alignment needs g = 8 rows of 4 per box and
+// measured slower (profiles/round1_ragged.jsonl).
+static uint64_t row_align(int es) { return es == 8 ? 32 : 16; }
+static uint64_t row_group(uint64_t pitch_bytes, int es) {  // row_align / gcd(pitch, row_align)
+  const uint64_t a = row_align(es);
+  uint64_t g = 1;
+  while (g < a && ((pitch_bytes * g) % a) != 0) g *= 2;
+  return g;
+}
+
+bool tma_group_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs) {
+  static int path = env_int("SLP_STORE_PATH", 0);
+  if (path == 2 || path == 3) return false;  // 3: staged instead of row groups (A/B)
+  const uint64_t seg = 128 / es;
+  const uint64_t g = row_group(ld_out * es, es);
+  return ((uintptr_t)out % es) == 0 && T >= (uint64_t)segs * seg + row_align(es) / es && ld_out >= T && nstreams >= g &&
+         g <= 8 &&
+         T < (1ull << 31) && g * ld_out * es < (1ull << 40) && nstreams < (1ull << 31);
+}
+
+int make_store_tmap_group(TmapGroup *tg, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out,
+                          int segs) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return SLP_ERR_CUDA;
+  }
+  const uint64_t g = row_group(ld_out * es, es);
+  const uint64_t seg = 128 / es;
+  const uintptr_t addr = (uintptr_t)out;
+  tg->g = (int)g;
+  tg->gsh = g == 8 ? 3 : (g == 4 ? 2 : (g == 2 ? 1 : 0));
+  tg->lead_max = 0;
+  for (int r = 0; r < 8; ++r) tg->lead[r] = 0;
+  for (uint64_t r = 0; r < g; ++r) {
+    const uintptr_t row = addr + r * ld_out * es;
+    const int lead = (int)(((row_align(es) - row % row_align(es)) % row_align(es)) / es);
+    tg->lead[r] = lead;
+    if (lead > tg->lead_max) tg->lead_max = lead;
+    cuuint64_t gdim[3] = {(cuuint64_t)seg, (cuuint64_t)((nstreams - r + g - 1) / g), (cuuint64_t)((T - lead) / seg)};
+    cuuint64_t gstride[2] = {(cuuint64_t)(g * ld_out * es), 128};
+    cuuint32_t box[3] = {(cuuint32_t)seg, (cuuint32_t)(32 / g), (cuuint32_t)segs};
+    cuuint32_t estride[3] = {1, 1, 1};
+    CUresult rc = fn(&tg->m[r], es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
+                     reinterpret_cast<void *>(row + lead * es), gdim, gstride, box, estride,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) {
+      set_last_error("cuTensorMapEncodeTiled (row groups) failed: " + std::to_string((int)rc));
+      return SLP_ERR_CUDA;
+    }
+  }
+  return SLP_OK;
+}
+
 namespace dev {
 __global__ void k_fused_final(const slp_checksum *parts, int nparts, slp_checksum *result, uint64_t count,
                               double fscale) {

@@ -22,6 +22,13 @@ namespace dev {
 //                64/128-byte pieces at only ~4.5-4.8 TB/s (profiles/wpattern.cu).
 //                With B buffers per warp, store i-B must have finished reading
 //                before tile i overwrites its buffer (cp.async.bulk.wait_group.read).
+//   FILL_TMA_G   stream-major rows that do not start 16-byte aligned (odd
+//                pitch, unaligned base; TmapGroup in slp_ops.h): row r first
+//                emits lead[r % g] outputs with element stores, so its tiles
+//                start aligned (32 B for u64); the tile keeps the rows of one parity
+//                together ([parity][seg][row / g][128 B], same swizzle) and
+//                leaves with g 3-D TMA stores (one per parity); the tail goes
+//                one output at a time through the tile;
 //   FILL_STAGED  stream-major, same staging, element stores (any pitch/alignment);
 //   FILL_POS     position-major: each output is one coalesced warp store
 //                (any pitch/alignment);
@@ -33,7 +40,15 @@ namespace dev {
 // Shared-memory tile layout [seg][row][128 B], chunk q of (seg, row) at
 // ((seg*32 + row) * 128) + ((q ^ (row & 7)) << 4)  (CU_TENSOR_MAP_SWIZZLE_128B).
 
-enum { FILL_TMA = 0, FILL_STAGED = 1, FILL_POS = 2, FILL_POS_TMA = 3 };
+enum { FILL_TMA = 0, FILL_STAGED = 1, FILL_POS = 2, FILL_POS_TMA = 3, FILL_TMA_G = 4 };
+template <int MODE>
+struct FillTmap {
+  using type = CUtensorMap;
+};
+template <>
+struct FillTmap<FILL_TMA_G> {
+  using type = TmapGroup;
+};
 constexpr int kFillThreads = kFillWarps * 32;
 
 // Fill tile configurations (slp_ops.h):
@@ -154,7 +169,8 @@ __device__ __forceinline__ void reduce_checksum_block(uint64_t slo, uint64_t shi
 }
 
 template <class G, int OK, int MODE, bool CSUM = false, bool SHORT = false, bool TAIL = false>
-__global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(kFillThreads)
+    k_fill(FillParams p, const __grid_constant__ typename FillTmap<MODE>::type tmap) {
   using word = typename G::word;
   using Cv = Out<OK, word>;
   using bits = typename Cv::bits;
@@ -172,6 +188,18 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
   constexpr int MSK = G::best_mask(0, 0);  // rotation pipe mix (ALU vs FMA), see Gen::best_mask
   const int lane = threadIdx.x & 31;
   const int warp = warp_uniform();  // keeps TMA coordinates in uniform registers
+  // shared-tile address of chunk q of piece seg of unit row r: [seg][row] or,
+  // for FILL_TMA_G, [parity][seg][row / g] (each parity is one TMA box)
+  auto taddr = [&](int seg, int r, int q) -> uint32_t {
+    if constexpr (MODE == FILL_TMA_G) {
+      const int row = ((r & (tmap.g - 1)) * kSegs + seg) * (32 >> tmap.gsh) + (r >> tmap.gsh);
+      return (row << 7) + ((q ^ (row & 7)) << 4);
+    } else {
+      return swz(seg, r, q);
+    }
+  };
+  int lead = 0;  // FILL_TMA_G: outputs of this lane's row before its first tile
+  if constexpr (MODE == FILL_TMA_G) lead = tmap.lead[lane & (tmap.g - 1)];
 
   extern __shared__ uint8_t smem_raw[];
   uint32_t tiles = 0;
@@ -181,7 +209,8 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
   const word *__restrict__ sin = static_cast<const word *>(p.sin);
   word *sout = static_cast<word *>(p.sout);
   bits *__restrict__ out = static_cast<bits *>(p.out);
-  const uint64_t ntiles = p.T / CH;
+  uint64_t ntiles = p.T / CH;
+  if constexpr (MODE == FILL_TMA_G) ntiles = (p.T - tmap.lead_max) / CH;  // tiles every row has after its lead
   const uint64_t rem = p.T - ntiles * CH;
   uint32_t issued = 0;  // tiles produced by this warp
   uint64_t cs_lo = 0, cs_hi = 0, cs_x = 0, cs_low = 0;  // CSUM accumulators (zero states emit zeros)
@@ -195,6 +224,16 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
 #pragma unroll
     for (int j = 0; j < K; ++j) dst[j] = ok ? sin[j * p.ld + st] : (word)0;
   };
+  // FILL_TMA_G: one 3-D store per row parity g (skipped where npieces[g] == 0)
+  // of the tile whose first piece is piece0 (counted after each row's lead)
+  auto store_groups = [&](uint32_t tile, uint64_t row0, uint64_t piece0, const int *npieces) {
+    if constexpr (MODE == FILL_TMA_G) {
+      for (int g = 0; g < tmap.g; ++g)
+        if (!npieces || npieces[g] > 0)
+          tma_store_3d(&tmap.m[g], tile + ((g * kSegs * (32 >> tmap.gsh)) << 7), 0, (int)(row0 >> tmap.gsh),
+                       (int)piece0);
+    }
+  };
   word nxt[K];
   load_states((uint64_t)blockIdx.x * kFillWarps + warp, nxt);
   for (uint64_t u = (uint64_t)blockIdx.x * kFillWarps + warp; u < p.nunits; u += ustride) {
@@ -205,6 +244,12 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
 #pragma unroll
     for (int j = 0; j < K; ++j) s[j] = nxt[j];
     load_states(u + ustride, nxt);
+    if constexpr (MODE == FILL_TMA_G) {  // the lead: this row's outputs before its 16-byte boundary
+      for (int t = 0; t < lead; ++t) {
+        const bits x = Cv::conv(G::next_flat(s));
+        if (valid) out[stream * p.ld_out + t] = x;
+      }
+    }
 
     // TAIL: a ragged row's last rem < CH outputs form one more tile; its
     // whole sub-blocks run through the same (rolled) code as a full tile
@@ -216,7 +261,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       bits *const pos_row = out + pos0 * p.ld_out + stream;  // FILL_POS: row pos0, this lane's column
       uint32_t tile = 0;
       auto wait_buffer = [&] {
-        if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA) {
+        if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA || MODE == FILL_TMA_G) {
           if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
         }
         __syncwarp();
@@ -237,7 +282,11 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
           return;
         }
         const int byte = e * ES;
-        const uint32_t addr = tile + ((b * ES / 128) << 12) + swz(byte >> 7, lane, (byte & 127) >> 4);
+        uint32_t addr;
+        if constexpr (MODE == FILL_TMA_G)
+          addr = tile + taddr((int)(b * ES / 128) + (byte >> 7), lane, (byte & 127) >> 4);
+        else
+          addr = tile + ((b * ES / 128) << 12) + swz(byte >> 7, lane, (byte & 127) >> 4);
         if constexpr (ES == 8) {
           asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(addr), "l"((uint64_t)v[0]), "l"((uint64_t)v[1])
                        : "memory");
@@ -365,6 +414,14 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
           bulk_commit();
         }
         ++issued;
+      } else if constexpr (MODE == FILL_TMA_G) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (elect_one()) {
+          store_groups(tile, row0, pos0 * ES / 128, nullptr);
+          bulk_commit();
+        }
+        ++issued;
 
       } else if constexpr (MODE == FILL_STAGED) {
         __syncwarp();
@@ -414,6 +471,73 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
           cs_low += (uint32_t)r & (G::w == 64 ? 0x7FFu : 0xFFu);
         }
         if (valid) out[(ntiles * CH + t) * p.ld_out + stream] = x;
+      }
+    } else if constexpr (MODE == FILL_TMA_G) {
+      // this row's last T - lead - ntiles*CH outputs (0 .. CH - 1 + lead_max):
+      // one at a time into the tile (past CH: element stores); per parity,
+      // whole pieces leave by TMA, the partial piece with element stores
+      const uint64_t done = ntiles * CH;
+      const uint32_t remr = (uint32_t)(p.T - lead - done);
+      const uint32_t rem_w = (uint32_t)(p.T - done);  // the largest (lead 0) in the warp
+      if (rem_w > 0) {
+        const uint32_t tile = tiles + (issued % kFillBufs) * kTileBytes;
+        if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
+        __syncwarp();
+        for (uint32_t t = 0; t < remr; ++t) {
+          const bits x = Cv::conv(G::next_flat(s));
+          if (t < (uint32_t)CH) {
+            const uint32_t byte = t * ES;
+            const uint32_t addr = tile + taddr(byte >> 7, lane, (byte & 127) >> 4) + (byte & 15);
+            if constexpr (ES == 8)
+              asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"((uint64_t)x) : "memory");
+            else
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"((uint32_t)x) : "memory");
+          } else if (valid) {
+            out[stream * p.ld_out + lead + done + t] = x;
+          }
+        }
+        constexpr int CPR = 128 / ES;  // elements per 128-byte piece
+        int npieces[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        bool any = false;
+        for (int g = 0; g < tmap.g; ++g) {
+          const uint64_t rg = p.T - tmap.lead[g] - done;
+          npieces[g] = (int)((rg < (uint64_t)CH ? rg : (uint64_t)CH) / CPR);
+          any |= npieces[g] > 0;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (any) {
+          if (elect_one()) {
+            store_groups(tile, row0, done * ES / 128, npieces);
+            bulk_commit();
+          }
+          ++issued;
+        }
+        // partial pieces: columns [npieces * CPR, min(rem, CH)) of each row
+        const uint32_t lim_w = rem_w < (uint32_t)CH ? rem_w : (uint32_t)CH;
+        constexpr int RPP = 32 / CPR;
+        const int nseg = (int)((lim_w + CPR - 1) / CPR);
+        for (int r0 = 0; r0 < 32 * nseg; r0 += RPP) {
+          const int rs = r0 + lane / CPR;  // (piece, row) flattened piece-major
+          const int seg = rs / 32, r = rs % 32;
+          const int e = lane % CPR;
+          const int rl = tmap.lead[r & (tmap.g - 1)];
+          const uint64_t rr = p.T - rl - done;
+          const uint64_t lim = rr < (uint64_t)CH ? rr : (uint64_t)CH;
+          const uint64_t col = (uint64_t)seg * CPR + e;
+          const uint64_t grow = row0 + r;
+          if (col >= (lim / CPR) * CPR && col < lim && grow < p.nstreams) {
+            bits v;
+            const uint32_t addr = tile + taddr(seg, r, (e * ES) >> 4) + (e * ES & 15);
+            if constexpr (ES == 8) {
+              asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+            } else {
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+            }
+            out[grow * p.ld_out + rl + done + col] = v;
+          }
+        }
+        __syncwarp();
       }
     } else if constexpr (TAIL) {
       if (rem > 0) {
@@ -531,7 +655,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(FillParams p, const __gri
       for (int j = 0; j < K; ++j) sout[j * p.ld + stream] = s[j];
     }
   }
-  if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA) {
+  if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA || MODE == FILL_TMA_G) {
     if (elect_one()) bulk_wait_all<0>();
   }
   if constexpr (CSUM) reduce_checksum_block<kFillWarps>(cs_lo, cs_hi, cs_x, cs_low, 0.0, p.partials);
@@ -652,10 +776,13 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
   if constexpr ((MODE == FILL_TMA || MODE == FILL_STAGED) && !CSUM && !TAIL) {
     if (p.T % (Shape::row_bytes / ES) != 0) return launch_fill<G, OK, MODE, false, SHORT, true>(p, st, grid_out);
   }
-  CUtensorMap tmap;
+  typename FillTmap<MODE>::type tmap;
   memset(&tmap, 0, sizeof tmap);
   if constexpr (MODE == FILL_TMA) {
     int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, Shape::segs);
+    if (rc != SLP_OK) return rc;
+  } else if constexpr (MODE == FILL_TMA_G) {
+    int rc = make_store_tmap_group(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, Shape::segs);
     if (rc != SLP_OK) return rc;
   } else if constexpr (MODE == FILL_POS_TMA) {
     int rc = make_store_tmap_pm(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out,
@@ -750,13 +877,18 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
   const bool short_rows = layout == SLP_STREAM_MAJOR && p.T < (uint64_t)segs * 128 / es;
   if (layout == SLP_STREAM_MAJOR) {
     const int ssegs = short_rows ? fill_cfg(0, FILL_KIND_SHORT).segs : segs;
-    mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, ssegs) ? FILL_TMA : FILL_STAGED;
+    mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, ssegs)
+               ? FILL_TMA
+               : (tma_group_ok(p.out, es, p.T, p.nstreams, p.ld_out, ssegs) ? FILL_TMA_G : FILL_STAGED);
   }
 #define SLP_FILL_CASE(OKV)                                                                              \
   if (ok == OKV) {                                                                                      \
     if (mode == FILL_TMA)                                                                               \
       return short_rows ? launch_fill<G, OKV, FILL_TMA, false, true>(p, st)                             \
                         : launch_fill<G, OKV, FILL_TMA>(p, st);                                         \
+    if (mode == FILL_TMA_G)                                                                             \
+      return short_rows ? launch_fill<G, OKV, FILL_TMA_G, false, true>(p, st)                           \
+                        : launch_fill<G, OKV, FILL_TMA_G>(p, st);                                       \
     if (mode == FILL_STAGED)                                                                            \
       return short_rows ? launch_fill<G, OKV, FILL_STAGED, false, true>(p, st)                          \
                         : launch_fill<G, OKV, FILL_STAGED>(p, st);                                      \

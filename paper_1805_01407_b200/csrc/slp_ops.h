@@ -126,4 +126,24 @@ bool tma_ok_pm(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t 
 int make_store_tmap_pm(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int ch,
                        int box_rows = 32);
 
+// Stream-major rows that do not start on a 16-byte boundary (odd T for
+// 8-byte outputs, T % 4 != 0 for 4-byte outputs, or an unaligned output
+// base).  A TMA box must start 16-byte aligned (profiles/tma_align_probe.cu),
+// and pieces that start inside a 32-byte sector leave partial sectors at
+// every tile boundary, so row r first emits lead[r % g] outputs with element
+// stores; its tiles then start on an a-byte boundary (a = 32 for 8-byte
+// outputs, 16 for 4-byte outputs).  Rows are taken in groups of
+// g = a / gcd(pitch, a): map p is a 3-D view (128-byte piece, row / g,
+// piece index) of the rows of parity p, based at row p's first aligned
+// output, with pitch g * pitch (a multiple of a), ceil((n - p) / g)
+// rows and (T - lead[p]) / (128 / es) whole pieces, so rows past the end and
+// partial pieces are clipped.
+struct alignas(64) TmapGroup {
+  CUtensorMap m[8];
+  int lead[8];  // outputs before the first tile, per parity
+  int g, gsh, lead_max;
+};
+bool tma_group_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);
+int make_store_tmap_group(TmapGroup *tg, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);
+
 }  // namespace slp
