@@ -48,3 +48,35 @@ def test_device_entry_points_reject_bad_arguments_without_touching_the_gpu():
     zero = (ctypes.c_uint64 * 4)()
     assert L.slp_jump_states(8, zero, 4, ctypes.c_void_p(16), 4, ctypes.c_void_p(16), 4, 4, None) \
         == _native.SLP_ERR_ZERO_STATE
+
+
+def test_more_entry_points_reject_bad_arguments_without_touching_the_gpu():
+    L = _native.lib()
+    E = _native
+    one = (ctypes.c_uint64 * 1)(1)
+    # segment split: unknown generator, nothing to do, null pointers, too many segments
+    assert L.slp_split_substreams(999, None, 1, 1, one, 1, 2, None, 2, None) == E.SLP_ERR_UNKNOWN_GENERATOR
+    assert L.slp_split_substreams(8, None, 1, 0, one, 1, 2, None, 2, None) == E.SLP_OK
+    assert L.slp_split_substreams(8, None, 1, 1, one, 1, 2, None, 2, None) == E.SLP_ERR_INVALID
+    assert L.slp_split_substreams(8, ctypes.c_void_p(16), 1, 1, one, 1, (1 << 20) + 1, ctypes.c_void_p(16),
+                                  (1 << 20) + 1, None) == E.SLP_ERR_INVALID
+    assert L.slp_split_substreams(8, ctypes.c_void_p(16), 1, 1, one, 1, 4, ctypes.c_void_p(16), 3, None) \
+        == E.SLP_ERR_INVALID  # ld_seg < n * J
+    # one LanedStream superbatch
+    assert L.slp_laned_fill(999, None, 1, 1, 0, None, None, None) == E.SLP_ERR_UNKNOWN_GENERATOR
+    assert L.slp_laned_fill(8, None, 0, 4, 0, None, None, None) == E.SLP_OK
+    assert L.slp_laned_fill(8, None, 4, 4, 0, None, None, None) == E.SLP_ERR_INVALID
+    # store + checksum: result / workspace required
+    assert L.slp_fill_checksum(999, None, None, 0, 0, 0, 0, None, 0, None, None, 0, None) \
+        == E.SLP_ERR_UNKNOWN_GENERATOR
+    assert L.slp_fill_checksum(8, None, None, 4, 4, 4, 0, None, 4, None, None, 0, None) == E.SLP_ERR_INVALID
+    # HWD counting: k out of range, split on a 32-bit generator, inconsistent range
+    cs = (ctypes.c_uint64 * 4)()
+    assert L.slp_hwd_count(8, ctypes.c_void_p(16), 1, 1, 1, 1, 0, 0, 0, 0, 64, 0, 0, cs, cs, None, None) \
+        == E.SLP_ERR_INVALID
+    w32 = L.slp_generator_id(b"xoshiro128starstar")
+    assert w32 >= 0
+    assert L.slp_hwd_count(w32, ctypes.c_void_p(16), 1, 1, 1, 1, 0, 0, 2, 0, 32, 0, 1, cs, cs, None, None) \
+        == E.SLP_ERR_INVALID
+    assert L.slp_hwd_count(8, ctypes.c_void_p(16), 1, 2, 10, 5, 0, 0, 2, 0, 64, 0, 0, cs, cs, None, None) \
+        == E.SLP_ERR_INVALID  # total <= (nthreads - 1) * tseg
