@@ -159,12 +159,22 @@ def cpu_baseline(steps_budget_s=20.0):
             tot += n
             secs += dt
             reps += 1
-        return {"value": tot / secs, "unit": UNIT, "cores": cb.procs, "kind": "port",
-                "sample": f"{reps} x ({cb.procs} procs x {lanes} substreams x {T} outputs) of config 2, "
-                          "numpy port of LanedStream lane set-up + VecStepper/apply_vec (oracle/cpu_baseline.py), "
-                          "lane set-up included"}
+        res = {"value": tot / secs, "unit": UNIT, "cores": cb.procs, "kind": "port",
+               "sample": f"{reps} x ({cb.procs} procs x {lanes} substreams x {T} outputs) of config 2, "
+                         "numpy port of LanedStream lane set-up + VecStepper/apply_vec (oracle/cpu_baseline.py), "
+                         "lane set-up included"}
     finally:
         cb.close()
+    # the same algorithm on one core (1-core and P-core figures)
+    c1 = CpuBaseline(GEN, SEED, T, procs=1)
+    try:
+        lanes1 = c1.calibrate(2.0)
+        n1, dt1 = c1.step(lanes1)
+        res["value_1core"] = n1 / dt1
+        res["sample_1core"] = f"1 proc x {lanes1} substreams x {T} outputs"
+    finally:
+        c1.close()
+    return res
 
 
 # ---------------------------------------------------------------- our arm
