@@ -166,9 +166,12 @@ def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor
     return out
 
 
-# the fill needs >= 2^18 substreams to reach its store rate; segments of
-# >= 2048 outputs and >= 8 per state bit amortise their jumps (profiles/
-# round1_split.jsonl)
+# One wave of the fill is 148 SMs x 7 warps x 32 = 33152 substreams; below
+# 2^15 substreams a long row is split into segments (up to 2^18 in all).
+# Segments of >= 2048 outputs and >= 8 per state bit amortise their jumps
+# (profiles/round1_split.jsonl, profiles/round1_shape_scan.jsonl: at 2^15
+# substreams and more the split only costs its jumps).
+SPLIT_MAX_N = 1 << 15
 SPLIT_TARGET_THREADS = 1 << 18
 SPLIT_MIN_SEG = 2048
 SPLIT_SEG_PER_BIT = 8
@@ -178,7 +181,7 @@ def _split_factor(spec: GeneratorSpec, n: int, T: int, layout: str, ld_out: int)
     """Segments per substream so that few, long substreams still fill the GPU.
     Only for contiguous stream-major output; each segment must be long enough
     to amortise its jump."""
-    if layout != "stream" or ld_out != T or n == 0 or n >= SPLIT_TARGET_THREADS // 2:
+    if layout != "stream" or ld_out != T or n == 0 or n >= SPLIT_MAX_N:
         return 1
     min_seg = max(SPLIT_MIN_SEG, SPLIT_SEG_PER_BIT * spec.kind.n)
     J = 1
