@@ -190,20 +190,27 @@ def _split_factor(spec: GeneratorSpec, n: int, T: int, layout: str, ld_out: int)
     return J
 
 
-def _fill_split(spec, gid, states, n, T, J, out, kind, sout, ld):
+def _split_states(spec, gid, states, ld, n, T, J):
     """Segment split (slp_split_substreams): substream i becomes J segments
-    i*J + j starting j*T/J steps ahead; their stream-major output with row
-    length T/J is byte-for-byte the output of the n substreams."""
-    k = spec.kind.k
+    i*J + j starting j*T/J steps ahead, as a (k, n*J) state tensor."""
+    seg = torch.empty((spec.kind.k, n * J), dtype=states.dtype, device=states.device)
+    sw, sn = _native.int_to_words(T // J)
+    with torch.cuda.device(states.device):
+        _native.check(_native.lib().slp_split_substreams(gid, ctypes.c_void_p(states.data_ptr()), ld, n, sw, sn, J,
+                                                         ctypes.c_void_p(seg.data_ptr()), n * J,
+                                                         _stream_ptr(states.device)), "split")
+    return seg
+
+
+def _fill_split(spec, gid, states, n, T, J, out, kind, sout, ld):
+    """The segments' stream-major output with row length T/J is byte-for-byte
+    the output of the n substreams."""
     dev = states.device
     seg_len = T // J
-    seg = torch.empty((k, n * J), dtype=states.dtype, device=dev)
-    sw, sn = _native.int_to_words(seg_len)
+    seg = _split_states(spec, gid, states, ld, n, T, J)
     L = _native.lib()
     stream = _stream_ptr(dev)
     with torch.cuda.device(dev):
-        _native.check(L.slp_split_substreams(gid, ctypes.c_void_p(states.data_ptr()), ld, n, sw, sn, J,
-                                             ctypes.c_void_p(seg.data_ptr()), n * J, stream), "split")
         _native.check(L.slp_fill(gid, ctypes.c_void_p(seg.data_ptr()), ctypes.c_void_p(seg.data_ptr()), n * J,
                                  n * J, seg_len, _KIND[kind], _native.STREAM_MAJOR,
                                  ctypes.c_void_p(out.data_ptr()), seg_len, stream), "fill")
@@ -248,6 +255,19 @@ def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, e
         result = torch.empty(_native.CHECKSUM_BYTES, dtype=torch.uint8, device=dev)
     flags = _native.FUSE_INT | (_native.FUSE_EXACT if exact else 0) | (_native.FUSE_F64 if f64 else 0)
     L = _native.lib()
+    J = _split_factor(spec, n, T, "stream", T)
+    if J > 1:
+        # few long substreams: the checksum is order-free, so reduce over the
+        # n*J segments of the split instead (float64 sum: same set, other order)
+        seg = _split_states(spec, gid, states, ld, n, T, J)
+        with torch.cuda.device(dev):
+            rc = L.slp_fused(gid, ctypes.c_void_p(seg.data_ptr()), ctypes.c_void_p(seg.data_ptr()), n * J, n * J,
+                             T // J, flags, ctypes.c_void_p(result.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                             ws.numel(), _stream_ptr(dev))
+        _native.check(rc, "fused")
+        if advance:
+            states[:, :n].copy_(seg[:, J - 1::J])  # substream i ends where its last segment ends
+        return result
     with torch.cuda.device(dev):
         rc = L.slp_fused(gid, ctypes.c_void_p(states.data_ptr()),
                          ctypes.c_void_p(states.data_ptr() if advance else None), ld, n, T, flags,
@@ -277,12 +297,19 @@ def fill_checksum(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: tor
     ws = _workspace(gid, dev)
     res = torch.empty(_native.CHECKSUM_BYTES, dtype=torch.uint8, device=dev)
     ld_out = out.stride(0) if n > 1 else T
+    J = _split_factor(spec, n, T, "stream", ld_out)
+    src, m, Tm, ldo = states, n, T, ld_out
+    if J > 1:  # few long substreams: store + checksum over the segments of the split
+        src = _split_states(spec, gid, states, n, n, T, J)
+        m, Tm, ldo = n * J, T // J, T // J
     with torch.cuda.device(dev):
-        rc = _native.lib().slp_fill_checksum(gid, ctypes.c_void_p(states.data_ptr()),
-                                             ctypes.c_void_p(states.data_ptr()), n, n, T, _KIND[kind],
-                                             ctypes.c_void_p(out.data_ptr()), ld_out,
+        rc = _native.lib().slp_fill_checksum(gid, ctypes.c_void_p(src.data_ptr()),
+                                             ctypes.c_void_p(src.data_ptr()), m, m, Tm, _KIND[kind],
+                                             ctypes.c_void_p(out.data_ptr()), ldo,
                                              ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
                                              ws.numel(), _stream_ptr(dev))
+    if J > 1 and rc == _native.SLP_OK:
+        states.copy_(src[:, J - 1::J])
     if rc == _native.SLP_ERR_UNSUPPORTED:
         c = fused_checksum(spec, states, T, exact=True, advance=False)
         fill(spec, states, T, out=out, kind=kind)

@@ -364,6 +364,40 @@ def test_segment_split_fill_is_transparent(name, n, T):
     assert torch.equal(a.states, ref.states)
 
 
+@pytest.mark.parametrize("name,n,T", [("xoshiro256starstar", 1, 1 << 20), ("xoroshiro1024plusplus", 3, 1 << 18),
+                                      ("xoshiro128starstar", 5, 1 << 17)])
+def test_segment_split_checksums_are_transparent(name, n, T):
+    """Few long substreams: the fused checksum (K4) and store + checksum (K2)
+    reduce over the segments of the split.  Exact fields and the advanced
+    states must equal the unsplit K4 pass (float64 sum: same set, other order)."""
+    import ctypes
+
+    from paper_1805_01407_b200 import _native
+
+    spec = P.get_spec(name)
+    assert D._split_factor(spec, n, T, "stream", T) > 1
+    ref = D.Substreams.from_seed(spec, 9, n)
+    res = torch.empty(_native.CHECKSUM_BYTES, dtype=torch.uint8, device="cuda")
+    ws = D._workspace(D.native_id(spec), ref.states.device)
+    flags = _native.FUSE_INT | _native.FUSE_EXACT | _native.FUSE_F64
+    rc = _native.lib().slp_fused(D.native_id(spec), ctypes.c_void_p(ref.states.data_ptr()),
+                                 ctypes.c_void_p(ref.states.data_ptr()), n, n, T, flags,
+                                 ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(), None)
+    assert rc == 0
+    want = D.decode_checksum(res, spec.kind.w, True, True)
+    a = D.Substreams.from_seed(spec, 9, n)
+    got = a.checksum(T, exact=True, f64=True)
+    assert (got.sum, got.xor, got.mant, got.count) == (want.sum, want.xor, want.mant, want.count)
+    assert abs(got.fsum_f64 - want.fsum_f64) <= 1e-12 * abs(want.fsum_f64)
+    assert torch.equal(a.states, ref.states)
+    b = D.Substreams.from_seed(spec, 9, n)
+    out, c = D.fill_checksum(spec, b.states, T)
+    assert (c.sum, c.xor, c.mant) == (want.sum, want.xor, want.mant)
+    assert torch.equal(b.states, ref.states)
+    d = D.Substreams.from_seed(spec, 9, n)
+    assert torch.equal(out, d.fill(T))
+
+
 @pytest.mark.parametrize("name,n,J", [("xoshiro256starstar", 1, 1 << 14), ("xoroshiro128plus", 3, 3000),
                                       ("xoshiro128plusplus", 40, 1500), ("xoroshiro1024starstar", 2, 1 << 12),
                                       ("xoshiro512plus", 5, 7), ("xoroshiro64star", 70000, 2)])
