@@ -132,6 +132,17 @@ int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *sr
 int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, const uint64_t *seg_steps,
                          int seg_words, uint64_t J, void *seg_states, uint64_t ld_seg, void *stream);
 
+/* Segments per substream that slp_fill (stream-major, ld_out == T),
+ * slp_fill_checksum and slp_fused use internally for n substreams of T
+ * outputs: 1 from 2^15 substreams up (one thread per substream fills the
+ * GPU), else the largest power of two J <= 2^18 / n dividing T with
+ * segments of >= max(2048, 8 * state bits) outputs.  The split runs in a
+ * stream-ordered scratch buffer (cudaMallocAsync); results are identical
+ * (checksums are order-free; the float64 sum covers the same set in another
+ * order).  SLP_SPLIT=0 in the environment disables it.  Returns J >= 1 or
+ * a negative status. */
+int64_t slp_split_factor(int id, uint64_t nstreams, uint64_t T);
+
 /* ---- device: bulk generation (kernels K2/K3/K5) ------------------------- */
 /* Emits T outputs of each of nstreams substreams (scramble current state,
  * then step: Generator.next, generators.py:244-305) into `out`, converting

@@ -76,6 +76,7 @@ SIGNATURES = {
                                            ctypes.c_uint64, ctypes.c_uint64, vp]),
     "slp_jump_states": (ctypes.c_int, [ctypes.c_int, u64p, ctypes.c_int, vp, ctypes.c_uint64, vp,
                                        ctypes.c_uint64, ctypes.c_uint64, vp]),
+    "slp_split_factor": (ctypes.c_int64, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64]),
     "slp_split_substreams": (ctypes.c_int, [ctypes.c_int, vp, ctypes.c_uint64, ctypes.c_uint64, u64p, ctypes.c_int,
                                             ctypes.c_uint64, vp, ctypes.c_uint64, vp]),
     "slp_fill": (ctypes.c_int, [ctypes.c_int, vp, vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,

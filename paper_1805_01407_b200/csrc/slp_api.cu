@@ -3,6 +3,7 @@
 // deterministic reduction of the fused consumer (K4).
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <stdexcept>
@@ -258,6 +259,14 @@ __global__ void k_fused_final(const slp_checksum *parts, int nparts, slp_checksu
     result->count = count;
     result->fsum = f * fscale;
   }
+}
+// states_out[j][i] = seg[j][i*J + J-1]: substream i ends where its last segment ends
+template <class W>
+__global__ void k_segment_ends(const W *seg, uint64_t n, uint64_t J, int k, W *out, uint64_t ld) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * (uint64_t)k) return;
+  const uint64_t j = t / n, i = t - j * n;
+  out[j * ld + i] = seg[j * n * J + i * J + J - 1];
 }
 }  // namespace dev
 
@@ -677,6 +686,76 @@ int slp_laned_fill(int id, const uint64_t *base_flat, uint64_t lanes, uint64_t l
   return slp_fill(id, states, states, lanes, lanes, lane_len, out_kind, SLP_STREAM_MAJOR, out, lane_len, stream);
 }
 
+// ---- few, long substreams: segment split --------------------------------------
+// One thread per substream fills the GPU only from about one wave of
+// substreams (148 SMs x 7 warps x 32 = 33152; profiles/round1_shape_scan.jsonl).
+// Below 2^15 substreams each is split into J segments i*J + j starting j*T/J
+// steps ahead (slp_split_substreams) in a stream-ordered scratch buffer: the
+// segment rows are byte-for-byte the substream rows, the checksums are
+// order-free, and substream i ends where segment i*J + J-1 ends.
+static uint64_t split_factor(const GenDesc &g, uint64_t n, uint64_t T) {
+  if (env_int("SLP_SPLIT", 1) == 0 || n == 0 || n >= (1ull << 15)) return 1;
+  const uint64_t min_seg = std::max<uint64_t>(2048, 8 * (uint64_t)g.n());
+  uint64_t J = 1;
+  while (n * J < (1ull << 18) && T % (2 * J) == 0 && T / (2 * J) >= min_seg) J *= 2;
+  return J;
+}
+
+int64_t slp_split_factor(int id, uint64_t nstreams, uint64_t T) {
+  const GenDesc *g = gen_desc(id);
+  if (!g) return SLP_ERR_UNKNOWN_GENERATOR;
+  return (int64_t)split_factor(*g, nstreams, T);
+}
+
+namespace {
+struct Segments {
+  void *states = nullptr;
+  cudaStream_t st = nullptr;
+  Segments() = default;
+  Segments(const Segments &) = delete;
+  Segments &operator=(const Segments &) = delete;
+  ~Segments() {
+    if (states) cudaFreeAsync(states, st);  // stream-ordered: after the kernels that use it
+  }
+};
+}  // namespace
+
+static int make_segments(int id, const GenDesc &g, const void *states, uint64_t ld, uint64_t n, uint64_t T,
+                         uint64_t J, cudaStream_t st, Segments &seg) {
+  seg.st = st;
+  const int dev = current_device();
+  static std::atomic<int> pool_set[64];
+  if (dev >= 0 && dev < 64 && !pool_set[dev]) {
+    // keep freed scratch in the device's default pool instead of unmapping it
+    // at every synchronisation (the default threshold, 0, costs ~1 ms a call)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = 1ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_set[dev] = 1;
+  }
+  if (cudaMallocAsync(&seg.states, (size_t)g.k * n * J * (g.w / 8), st) != cudaSuccess) {
+    seg.states = nullptr;
+    return cuda_fail("cudaMallocAsync(segments)");
+  }
+  const uint64_t steps[1] = {T / J};
+  return slp_split_substreams(id, states, ld, n, steps, 1, J, seg.states, n * J, st);
+}
+
+static int segment_ends(const GenDesc &g, const Segments &seg, uint64_t n, uint64_t J, void *states_out, uint64_t ld,
+                        cudaStream_t st) {
+  const uint64_t total = n * (uint64_t)g.k;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  if (g.w == 64)
+    slp::dev::k_segment_ends<uint64_t><<<blocks, 256, 0, st>>>(static_cast<const uint64_t *>(seg.states), n, J, g.k,
+                                                          static_cast<uint64_t *>(states_out), ld);
+  else
+    slp::dev::k_segment_ends<uint32_t><<<blocks, 256, 0, st>>>(static_cast<const uint32_t *>(seg.states), n, J, g.k,
+                                                          static_cast<uint32_t *>(states_out), ld);
+  return check_launch("k_segment_ends");
+}
+
 int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams, uint64_t T,
              int out_kind, int layout, void *out, uint64_t ld_out, void *stream) {
   const GenDesc *g = gen_desc(id);
@@ -708,7 +787,21 @@ int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint6
     }
     return SLP_OK;
   }
-  return ops->fill(p, out_kind, layout, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t J = layout == SLP_STREAM_MAJOR && ld_out == T ? split_factor(*g, nstreams, T) : 1;
+  if (J > 1) {
+    Segments seg;
+    int rc = make_segments(id, *g, states_in, ld, nstreams, T, J, st, seg);
+    if (rc != SLP_OK) return rc;
+    FillParams q = p;
+    q.sin = q.sout = seg.states;
+    q.ld = q.nstreams = nstreams * J;
+    q.T = q.ld_out = T / J;
+    rc = ops->fill(q, out_kind, layout, st);
+    if (rc != SLP_OK || !states_out) return rc;
+    return segment_ends(*g, seg, nstreams, J, states_out, ld, st);
+  }
+  return ops->fill(p, out_kind, layout, st);
 }
 
 int slp_fill_checksum(int id, const void *states_in, void *states_out, uint64_t ld, uint64_t nstreams, uint64_t T,
@@ -733,8 +826,22 @@ int slp_fill_checksum(int id, const void *states_in, void *states_out, uint64_t 
     p.ld_out = ld_out;
     p.partials = workspace;
     p.workspace_bytes = workspace_bytes;
-    const int rc = ops->fill_csum(p, out_kind, st, &grid);
-    if (rc != SLP_OK) return rc;
+    const uint64_t J = ld_out == T ? split_factor(*g, nstreams, T) : 1;
+    if (J > 1) {
+      Segments seg;
+      int rc = make_segments(id, *g, states_in, ld, nstreams, T, J, st, seg);
+      if (rc != SLP_OK) return rc;
+      FillParams q = p;
+      q.sin = q.sout = seg.states;
+      q.ld = q.nstreams = nstreams * J;
+      q.T = q.ld_out = T / J;
+      rc = ops->fill_csum(q, out_kind, st, &grid);
+      if (rc == SLP_OK && states_out) rc = segment_ends(*g, seg, nstreams, J, states_out, ld, st);
+      if (rc != SLP_OK) return rc;
+    } else {
+      const int rc = ops->fill_csum(p, out_kind, st, &grid);
+      if (rc != SLP_OK) return rc;
+    }
   }
   const double fscale = g->w == 64 ? 0x1.0p-53 : 0x1.0p-24;
   dev::k_fused_final<<<1, 256, 0, st>>>(static_cast<const slp_checksum *>(workspace), grid,
@@ -770,7 +877,21 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
   p.one = 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int grid = 0;
-  int rc = ops->fused(p, flags, st, &grid);
+  int rc;
+  const uint64_t J = split_factor(*g, nstreams, T);
+  if (J > 1) {
+    Segments seg;
+    rc = make_segments(id, *g, states_in, ld, nstreams, T, J, st, seg);
+    if (rc != SLP_OK) return rc;
+    FusedParams q = p;
+    q.sin = q.sout = seg.states;
+    q.ld = q.nstreams = nstreams * J;
+    q.T = T / J;
+    rc = ops->fused(q, flags, st, &grid);
+    if (rc == SLP_OK && states_out) rc = segment_ends(*g, seg, nstreams, J, states_out, ld, st);
+  } else {
+    rc = ops->fused(p, flags, st, &grid);
+  }
   if (rc != SLP_OK) return rc;
   const double fscale = g->w == 64 ? 0x1.0p-53 : 0x1.0p-24;
   dev::k_fused_final<<<1, 256, 0, st>>>(static_cast<const slp_checksum *>(workspace), grid,

@@ -154,10 +154,6 @@ def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor
             raise ValueError("states_out must match states (shape, dtype, strides)")
         sout = states_out.data_ptr()
     L = _native.lib()
-    J = _split_factor(spec, n, T, layout, ld_out)
-    if J > 1:
-        wb = None if sout is None else (states if states_out is None else states_out)
-        return _fill_split(spec, gid, states, n, T, J, out, kind, wb, ld)
     with torch.cuda.device(states.device):
         rc = L.slp_fill(gid, ctypes.c_void_p(states.data_ptr()), ctypes.c_void_p(sout), ld, n, T,
                         _KIND[kind], _LAYOUT[layout], ctypes.c_void_p(out.data_ptr()), ld_out,
@@ -166,57 +162,12 @@ def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor
     return out
 
 
-# One wave of the fill is 148 SMs x 7 warps x 32 = 33152 substreams; below
-# 2^15 substreams a long row is split into segments (up to 2^18 in all).
-# Segments of >= 2048 outputs and >= 8 per state bit amortise their jumps
-# (profiles/round1_split.jsonl, profiles/round1_shape_scan.jsonl: at 2^15
-# substreams and more the split only costs its jumps).
-SPLIT_MAX_N = 1 << 15
-SPLIT_TARGET_THREADS = 1 << 18
-SPLIT_MIN_SEG = 2048
-SPLIT_SEG_PER_BIT = 8
-
-
 def _split_factor(spec: GeneratorSpec, n: int, T: int, layout: str, ld_out: int) -> int:
-    """Segments per substream so that few, long substreams still fill the GPU.
-    Only for contiguous stream-major output; each segment must be long enough
-    to amortise its jump."""
-    if layout != "stream" or ld_out != T or n == 0 or n >= SPLIT_MAX_N:
+    """Segments per substream the C ABI uses internally for few, long
+    substreams (slp_split_factor; stream-major contiguous rows only)."""
+    if layout != "stream" or ld_out != T:
         return 1
-    min_seg = max(SPLIT_MIN_SEG, SPLIT_SEG_PER_BIT * spec.kind.n)
-    J = 1
-    while n * J < SPLIT_TARGET_THREADS and T % (2 * J) == 0 and T // (2 * J) >= min_seg:
-        J *= 2
-    return J
-
-
-def _split_states(spec, gid, states, ld, n, T, J):
-    """Segment split (slp_split_substreams): substream i becomes J segments
-    i*J + j starting j*T/J steps ahead, as a (k, n*J) state tensor."""
-    seg = torch.empty((spec.kind.k, n * J), dtype=states.dtype, device=states.device)
-    sw, sn = _native.int_to_words(T // J)
-    with torch.cuda.device(states.device):
-        _native.check(_native.lib().slp_split_substreams(gid, ctypes.c_void_p(states.data_ptr()), ld, n, sw, sn, J,
-                                                         ctypes.c_void_p(seg.data_ptr()), n * J,
-                                                         _stream_ptr(states.device)), "split")
-    return seg
-
-
-def _fill_split(spec, gid, states, n, T, J, out, kind, sout, ld):
-    """The segments' stream-major output with row length T/J is byte-for-byte
-    the output of the n substreams."""
-    dev = states.device
-    seg_len = T // J
-    seg = _split_states(spec, gid, states, ld, n, T, J)
-    L = _native.lib()
-    stream = _stream_ptr(dev)
-    with torch.cuda.device(dev):
-        _native.check(L.slp_fill(gid, ctypes.c_void_p(seg.data_ptr()), ctypes.c_void_p(seg.data_ptr()), n * J,
-                                 n * J, seg_len, _KIND[kind], _native.STREAM_MAJOR,
-                                 ctypes.c_void_p(out.data_ptr()), seg_len, stream), "fill")
-    if sout is not None:
-        sout[:, :n].copy_(seg[:, J - 1::J])  # substream i ends where its last segment ends
-    return out
+    return int(_native.lib().slp_split_factor(native_id(spec), n, T))
 
 
 _ws_bytes: dict = {}
@@ -255,19 +206,6 @@ def fused_checksum_async(spec: GeneratorSpec, states: torch.Tensor, T: int, *, e
         result = torch.empty(_native.CHECKSUM_BYTES, dtype=torch.uint8, device=dev)
     flags = _native.FUSE_INT | (_native.FUSE_EXACT if exact else 0) | (_native.FUSE_F64 if f64 else 0)
     L = _native.lib()
-    J = _split_factor(spec, n, T, "stream", T)
-    if J > 1:
-        # few long substreams: the checksum is order-free, so reduce over the
-        # n*J segments of the split instead (float64 sum: same set, other order)
-        seg = _split_states(spec, gid, states, ld, n, T, J)
-        with torch.cuda.device(dev):
-            rc = L.slp_fused(gid, ctypes.c_void_p(seg.data_ptr()), ctypes.c_void_p(seg.data_ptr()), n * J, n * J,
-                             T // J, flags, ctypes.c_void_p(result.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
-                             ws.numel(), _stream_ptr(dev))
-        _native.check(rc, "fused")
-        if advance:
-            states[:, :n].copy_(seg[:, J - 1::J])  # substream i ends where its last segment ends
-        return result
     with torch.cuda.device(dev):
         rc = L.slp_fused(gid, ctypes.c_void_p(states.data_ptr()),
                          ctypes.c_void_p(states.data_ptr() if advance else None), ld, n, T, flags,
@@ -297,19 +235,12 @@ def fill_checksum(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: tor
     ws = _workspace(gid, dev)
     res = torch.empty(_native.CHECKSUM_BYTES, dtype=torch.uint8, device=dev)
     ld_out = out.stride(0) if n > 1 else T
-    J = _split_factor(spec, n, T, "stream", ld_out)
-    src, m, Tm, ldo = states, n, T, ld_out
-    if J > 1:  # few long substreams: store + checksum over the segments of the split
-        src = _split_states(spec, gid, states, n, n, T, J)
-        m, Tm, ldo = n * J, T // J, T // J
     with torch.cuda.device(dev):
-        rc = _native.lib().slp_fill_checksum(gid, ctypes.c_void_p(src.data_ptr()),
-                                             ctypes.c_void_p(src.data_ptr()), m, m, Tm, _KIND[kind],
-                                             ctypes.c_void_p(out.data_ptr()), ldo,
+        rc = _native.lib().slp_fill_checksum(gid, ctypes.c_void_p(states.data_ptr()),
+                                             ctypes.c_void_p(states.data_ptr()), n, n, T, _KIND[kind],
+                                             ctypes.c_void_p(out.data_ptr()), ld_out,
                                              ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
                                              ws.numel(), _stream_ptr(dev))
-    if J > 1 and rc == _native.SLP_OK:
-        states.copy_(src[:, J - 1::J])
     if rc == _native.SLP_ERR_UNSUPPORTED:
         c = fused_checksum(spec, states, T, exact=True, advance=False)
         fill(spec, states, T, out=out, kind=kind)

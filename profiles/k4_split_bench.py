@@ -1,5 +1,5 @@
 """Fused checksum (K4) of few long substreams, with and without the segment split
-(D.SPLIT_MAX_N = 0 disables it).  One JSON line per case."""
+(SLP_SPLIT=0 disables it; read on every call).  One JSON line per case."""
 import sys, json, os
 sys.path.insert(0, os.getcwd())
 import torch
@@ -9,7 +9,7 @@ for name in ["xoshiro256starstar", "xoroshiro1024plusplus"]:
     spec = P.get_spec(name)
     for n, T in [(1, 1 << 28), (16, 1 << 24), (1000, 1 << 18)]:
         for split in (True, False):
-            D.SPLIT_MAX_N = (1 << 15) if split else 0
+            os.environ["SLP_SPLIT"] = "1" if split else "0"
             sub = D.Substreams.from_seed(spec, 42, n)
             sub.checksum(T)
             torch.cuda.synchronize()

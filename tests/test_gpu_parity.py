@@ -347,6 +347,8 @@ def test_edge_laned_geometries(lanes, lane_len, total):
 def test_segment_split_fill_is_transparent(name, n, T):
     """Few, long substreams are split into jumped segments on the device; the
     output and the advanced states must equal the unsplit computation."""
+    import os
+
     spec = P.get_spec(name)
     assert D._split_factor(spec, n, T, "stream", T) > 1
     a = D.Substreams.from_seed(spec, 5, n)
@@ -355,9 +357,13 @@ def test_segment_split_fill_is_transparent(name, n, T):
     want = torch.empty_like(out)
     L = __import__("paper_1805_01407_b200._native", fromlist=["x"])
     import ctypes
-    rc = L.lib().slp_fill(D.native_id(spec), ctypes.c_void_p(ref.states.data_ptr()),
-                          ctypes.c_void_p(ref.states.data_ptr()), n, n, T, 0, 0,
-                          ctypes.c_void_p(want.data_ptr()), T, None)
+    os.environ["SLP_SPLIT"] = "0"  # the unsplit fill: one thread per substream
+    try:
+        rc = L.lib().slp_fill(D.native_id(spec), ctypes.c_void_p(ref.states.data_ptr()),
+                              ctypes.c_void_p(ref.states.data_ptr()), n, n, T, 0, 0,
+                              ctypes.c_void_p(want.data_ptr()), T, None)
+    finally:
+        del os.environ["SLP_SPLIT"]
     assert rc == 0
     torch.cuda.synchronize()
     assert torch.equal(out, want)
@@ -368,8 +374,9 @@ def test_segment_split_fill_is_transparent(name, n, T):
                                       ("xoshiro128starstar", 5, 1 << 17)])
 def test_segment_split_checksums_are_transparent(name, n, T):
     """Few long substreams: the fused checksum (K4) and store + checksum (K2)
-    reduce over the segments of the split.  Exact fields and the advanced
-    states must equal the unsplit K4 pass (float64 sum: same set, other order)."""
+    reduce over the segments of the split (inside the C ABI).  Exact fields
+    and the advanced states must equal the unsplit K4 pass (SLP_SPLIT=0;
+    float64 sum: same set, other order)."""
     import ctypes
 
     from paper_1805_01407_b200 import _native
@@ -380,9 +387,17 @@ def test_segment_split_checksums_are_transparent(name, n, T):
     res = torch.empty(_native.CHECKSUM_BYTES, dtype=torch.uint8, device="cuda")
     ws = D._workspace(D.native_id(spec), ref.states.device)
     flags = _native.FUSE_INT | _native.FUSE_EXACT | _native.FUSE_F64
-    rc = _native.lib().slp_fused(D.native_id(spec), ctypes.c_void_p(ref.states.data_ptr()),
-                                 ctypes.c_void_p(ref.states.data_ptr()), n, n, T, flags,
-                                 ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(), None)
+    import os
+
+    os.environ["SLP_SPLIT"] = "0"  # the unsplit K4 pass: one thread per substream
+    try:
+        rc = _native.lib().slp_fused(D.native_id(spec), ctypes.c_void_p(ref.states.data_ptr()),
+                                     ctypes.c_void_p(ref.states.data_ptr()), n, n, T, flags,
+                                     ctypes.c_void_p(res.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                     None)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["SLP_SPLIT"]
     assert rc == 0
     want = D.decode_checksum(res, spec.kind.w, True, True)
     a = D.Substreams.from_seed(spec, 9, n)
