@@ -80,3 +80,19 @@ def test_more_entry_points_reject_bad_arguments_without_touching_the_gpu():
         == E.SLP_ERR_INVALID
     assert L.slp_hwd_count(8, ctypes.c_void_p(16), 1, 2, 10, 5, 0, 0, 2, 0, 64, 0, 0, cs, cs, None, None) \
         == E.SLP_ERR_INVALID  # total <= (nthreads - 1) * tseg
+
+
+def test_split_factor_is_host_only_and_follows_the_wave_rule():
+    """slp_split_factor (no device call): 1 from 2^15 substreams up or for
+    rows too short to split; else a power of two with segments >= 2048
+    outputs and n*J <= 2^18."""
+    L = _native.lib()
+    g = L.slp_generator_id(b"xoshiro256starstar")
+    assert L.slp_split_factor(999, 1, 1 << 20) == _native.SLP_ERR_UNKNOWN_GENERATOR
+    assert L.slp_split_factor(g, 1 << 15, 1 << 20) == 1
+    assert L.slp_split_factor(g, 1000, 4095) == 1
+    for n, T in [(1, 1 << 28), (16, 1 << 24), (1000, 1 << 18), (3, 3 << 16)]:
+        J = L.slp_split_factor(g, n, T)
+        assert J > 1 and J & (J - 1) == 0 and T % J == 0 and T // J >= 2048 and n * J <= 1 << 18
+    big = L.slp_generator_id(b"xoroshiro1024starstar")
+    assert (1 << 20) // L.slp_split_factor(big, 1, 1 << 20) >= 8 * 1024  # >= 8 outputs per state bit
