@@ -253,11 +253,15 @@ __global__ void __launch_bounds__(kFillThreads)
 
     // TAIL: a ragged row's last rem < CH outputs form one more tile; its
     // whole sub-blocks run through the same (rolled) code as a full tile
-    const uint64_t nloop = ntiles + (TAIL && rem >= (uint64_t)U ? 1 : 0);
+    // (FILL_TMA_G: the same for the tail every row of the warp has after its lead)
+    constexpr bool TAIL_LOOP = TAIL || MODE == FILL_TMA_G;
+    uint64_t rem_loop = rem;
+    if constexpr (MODE == FILL_TMA_G) rem_loop = p.T - tmap.lead_max - ntiles * CH;
+    const uint64_t nloop = ntiles + (TAIL_LOOP && rem_loop >= (uint64_t)U ? 1 : 0);
     uint32_t tail_tile = 0;
     for (uint64_t c = 0; c < nloop; ++c) {
       const uint64_t pos0 = c * CH;
-      const uint32_t sub_end = (!TAIL || c < ntiles) ? (uint32_t)CH : (uint32_t)(rem / U) * U;
+      const uint32_t sub_end = (!TAIL_LOOP || c < ntiles) ? (uint32_t)CH : (uint32_t)(rem_loop / U) * U;
       bits *const pos_row = out + pos0 * p.ld_out + stream;  // FILL_POS: row pos0, this lane's column
       uint32_t tile = 0;
       auto wait_buffer = [&] {
@@ -392,7 +396,7 @@ __global__ void __launch_bounds__(kFillThreads)
         cs_x ^= (uint64_t)t_x;
         cs_low += t_low;
       }
-      if constexpr (TAIL) {
+      if constexpr (TAIL_LOOP) {
         if (c == ntiles) {  // the tail tile: completed and stored below
           tail_tile = tile;
           break;
@@ -474,16 +478,22 @@ __global__ void __launch_bounds__(kFillThreads)
       }
     } else if constexpr (MODE == FILL_TMA_G) {
       // this row's last T - lead - ntiles*CH outputs (0 .. CH - 1 + lead_max):
-      // one at a time into the tile (past CH: element stores); per parity,
-      // whole pieces leave by TMA, the partial piece with element stores
+      // whole sub-blocks through the tile loop, the rest one at a time into
+      // the tile (past CH: element stores); per parity, whole pieces leave by
+      // TMA, the partial piece with element stores
       const uint64_t done = ntiles * CH;
       const uint32_t remr = (uint32_t)(p.T - lead - done);
       const uint32_t rem_w = (uint32_t)(p.T - done);  // the largest (lead 0) in the warp
       if (rem_w > 0) {
-        const uint32_t tile = tiles + (issued % kFillBufs) * kTileBytes;
-        if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
-        __syncwarp();
-        for (uint32_t t = 0; t < remr; ++t) {
+        // whole sub-blocks common to every row already ran in the tile loop
+        const uint32_t rb = rem_loop >= (uint64_t)U ? (uint32_t)(rem_loop / U) * U : 0u;
+        uint32_t tile = tail_tile;
+        if (rb == 0) {
+          tile = tiles + (issued % kFillBufs) * kTileBytes;
+          if (issued >= kFillBufs && elect_one()) bulk_wait_read<kFillBufs - 1>();
+          __syncwarp();
+        }
+        for (uint32_t t = rb; t < remr; ++t) {
           const bits x = Cv::conv(G::next_flat(s));
           if (t < (uint32_t)CH) {
             const uint32_t byte = t * ES;
