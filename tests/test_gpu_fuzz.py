@@ -148,3 +148,35 @@ def test_hwd_counts_fuzz(seed):
         msg = f"{name} k={k} {mode} split={split} [{c0}, {c1})"
         np.testing.assert_array_equal(got_c, want_c, err_msg=msg)
         np.testing.assert_array_equal(got_s, want_s, err_msg=msg)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SLP_FUZZ_SEEDS", "12")) // 3 + 1))
+def test_split_fuzz(seed):
+    """Few long substreams (segment split inside the C ABI) on random
+    generators, counts and row lengths: fill, store + checksum and the fused
+    checksum against the oracle, with the advanced states."""
+    rng = np.random.default_rng(11000 + seed)
+    for _ in range(3):
+        name = ALL[rng.integers(len(ALL))]
+        spec = P.get_spec(name)
+        w = spec.kind.w
+        n = int(rng.choice([1, 2, 3, 7]))
+        T = int(rng.choice([4096, 8192, 3 * 4096, 1 << 15]))
+        if D._split_factor(spec, n, T, "stream", T) == 1:
+            continue
+        flat = rng.integers(0, 1 << 63, size=(spec.kind.k, n), dtype=np.uint64) | np.uint64(1)
+        if w == 32:
+            flat &= np.uint64(0xFFFFFFFF)
+        want, want_S = O.vec_outputs(name, flat, T)
+        msg = f"{name} n={n} T={T}"
+        sub = D.Substreams.from_states(spec, flat)
+        got = D.fill(spec, sub.states, T).cpu().numpy()
+        np.testing.assert_array_equal(got.astype(np.uint64), want.astype(np.uint64), err_msg=msg)
+        np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S, err_msg=msg)
+        oc = O.checksum(want, w)
+        c = D.Substreams.from_states(spec, flat).checksum(T, exact=True)
+        assert (c.sum, c.xor, c.mant) == (oc["sum"], oc["xor"], oc["mant"]), msg
+        sub2 = D.Substreams.from_states(spec, flat)
+        _, c2 = D.fill_checksum(spec, sub2.states, T)
+        assert (c2.sum, c2.xor, c2.mant) == (oc["sum"], oc["xor"], oc["mant"]), msg
+        np.testing.assert_array_equal(sub2.states.cpu().numpy().astype(np.uint64), want_S, err_msg=msg)
