@@ -135,8 +135,9 @@ int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, co
 /* Segments per substream that slp_fill (stream-major, ld_out == T),
  * slp_fill_checksum and slp_fused use internally for n substreams of T
  * outputs: 1 from 2^15 substreams up (one thread per substream fills the
- * GPU), else the largest power of two J <= 2^18 / n dividing T with
- * segments of >= max(2048, 8 * state bits) outputs.  The split runs in a
+ * GPU); else a power of two J dividing T, doubled up to n*J = 2^14 while
+ * segments keep >= max(512, 2 * state bits) outputs, then up to 2^18 while
+ * they keep >= max(2048, 8 * state bits).  The split runs in a
  * stream-ordered scratch buffer (cudaMallocAsync); results are identical
  * (checksums are order-free; the float64 sum covers the same set in another
  * order).  SLP_SPLIT=0 in the environment disables it.  Returns J >= 1 or

@@ -693,11 +693,18 @@ int slp_laned_fill(int id, const uint64_t *base_flat, uint64_t lanes, uint64_t l
 // steps ahead (slp_split_substreams) in a stream-ordered scratch buffer: the
 // segment rows are byte-for-byte the substream rows, the checksums are
 // order-free, and substream i ends where segment i*J + J-1 ends.
+// J doubles first up to half a wave of segments (2^14) while they keep
+// >= max(512, 2 * state bits) outputs, then up to 2^18 segments while they
+// keep >= max(2048, 8 * state bits) (long rows: more parallelism, jumps
+// amortised).  A full first-phase wave measured slower: its extra jumps
+// cost more than the fill gains (profiles/round1_shape_scan.jsonl).
 static uint64_t split_factor(const GenDesc &g, uint64_t n, uint64_t T) {
   if (env_int("SLP_SPLIT", 1) == 0 || n == 0 || n >= (1ull << 15)) return 1;
-  const uint64_t min_seg = std::max<uint64_t>(2048, 8 * (uint64_t)g.n());
+  const uint64_t bits = (uint64_t)g.n();
+  const uint64_t min_wave = std::max<uint64_t>(512, 2 * bits), min_long = std::max<uint64_t>(2048, 8 * bits);
   uint64_t J = 1;
-  while (n * J < (1ull << 18) && T % (2 * J) == 0 && T / (2 * J) >= min_seg) J *= 2;
+  while (n * J < (1ull << 14) && T % (2 * J) == 0 && T / (2 * J) >= min_wave) J *= 2;
+  while (n * J < (1ull << 18) && T % (2 * J) == 0 && T / (2 * J) >= min_long) J *= 2;
   return J;
 }
 

@@ -84,15 +84,18 @@ def test_more_entry_points_reject_bad_arguments_without_touching_the_gpu():
 
 def test_split_factor_is_host_only_and_follows_the_wave_rule():
     """slp_split_factor (no device call): 1 from 2^15 substreams up or for
-    rows too short to split; else a power of two with segments >= 2048
-    outputs and n*J <= 2^18."""
+    rows too short to split; else a power of two: segments >= 512 outputs up
+    to half a wave (2^14 segments), >= 2048 beyond, n*J <= 2^18."""
     L = _native.lib()
     g = L.slp_generator_id(b"xoshiro256starstar")
     assert L.slp_split_factor(999, 1, 1 << 20) == _native.SLP_ERR_UNKNOWN_GENERATOR
     assert L.slp_split_factor(g, 1 << 15, 1 << 20) == 1
-    assert L.slp_split_factor(g, 1000, 4095) == 1
-    for n, T in [(1, 1 << 28), (16, 1 << 24), (1000, 1 << 18), (3, 3 << 16)]:
+    assert L.slp_split_factor(g, 1000, 1023) == 1
+    for n, T in [(1, 1 << 28), (16, 1 << 24), (1000, 1 << 18), (3, 3 << 16), (4096, 4096), (8192, 2048)]:
         J = L.slp_split_factor(g, n, T)
-        assert J > 1 and J & (J - 1) == 0 and T % J == 0 and T // J >= 2048 and n * J <= 1 << 18
+        assert J > 1 and J & (J - 1) == 0 and T % J == 0 and T // J >= 512 and n * J <= 1 << 18
+        assert T // J >= 2048 or n * J <= 1 << 14
+    assert L.slp_split_factor(g, 4096, 4096) == 4 and L.slp_split_factor(g, 1, 1 << 28) == 1 << 17
     big = L.slp_generator_id(b"xoroshiro1024starstar")
-    assert (1 << 20) // L.slp_split_factor(big, 1, 1 << 20) >= 8 * 1024  # >= 8 outputs per state bit
+    assert (1 << 20) // L.slp_split_factor(big, 1, 1 << 20) >= 2 * 1024  # >= 2 outputs per state bit
+    assert (1 << 28) // L.slp_split_factor(big, 1, 1 << 28) >= 8 * 1024  # long rows: >= 8 per state bit
