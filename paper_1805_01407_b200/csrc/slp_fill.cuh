@@ -25,10 +25,11 @@ namespace dev {
 //   FILL_TMA_G   stream-major rows that do not start 16-byte aligned (odd
 //                pitch, unaligned base; TmapGroup in slp_ops.h): row r first
 //                emits lead[r % g] outputs with element stores, so its tiles
-//                start aligned (32 B for u64); the tile keeps the rows of one parity
-//                together ([parity][seg][row / g][128 B], same swizzle) and
-//                leaves with g 3-D TMA stores (one per parity); the tail goes
-//                one output at a time through the tile;
+//                start aligned (32 B for u64); the tile keeps the rows of
+//                one parity together ([parity][seg][row / g][128 B], same
+//                swizzle) and leaves with g 3-D TMA stores (one per parity);
+//                the tail's common sub-blocks run through the tile loop, the
+//                rest one output at a time into the same tile;
 //   FILL_STAGED  stream-major, same staging, element stores (any pitch/alignment);
 //   FILL_POS     position-major: each output is one coalesced warp store
 //                (any pitch/alignment);
