@@ -54,3 +54,20 @@ def test_criterion11_default_jumps_ten_seeds(name):
         g2 = P.Generator.from_seed(spec, seed)
         g2.jump(long_jump)
         assert list(g2.flat_words()) == O.jump(name, flat, plj), (name, seed)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,lanes,lane_len", [("xoshiro256starstar", 512, 8192), ("xoroshiro128plus", 64, 1 << 14),
+                                                 ("xoshiro128starstar", 256, 4096)])
+def test_laned_stream_through_the_segment_split(name, lanes, lane_len):
+    """LanedStream geometries below one wave of lanes: the C ABI splits every
+    lane into jumped segments; two superbatches (super-jump between them)
+    must still equal the reference's laned stream."""
+    from paper_1805_01407_b200 import device as D
+
+    spec = P.get_spec(name)
+    assert D._split_factor(spec, lanes, lane_len, "stream", lane_len) > 1
+    total = 2 * lanes * lane_len - 777
+    want = O.laned_stream(name, 5, total, lanes, lane_len)
+    got = np.concatenate(list(P.output_stream(spec, seed=5, total_values=total, lanes=lanes, lane_len=lane_len)))
+    np.testing.assert_array_equal(got, want)
