@@ -698,8 +698,8 @@ int slp_laned_fill(int id, const uint64_t *base_flat, uint64_t lanes, uint64_t l
 // keep >= max(2048, 8 * state bits) (long rows: more parallelism, jumps
 // amortised).  A full first-phase wave measured slower: its extra jumps
 // cost more than the fill gains (profiles/round1_shape_scan.jsonl).
-static uint64_t split_factor(const GenDesc &g, uint64_t n, uint64_t T) {
-  if (env_int("SLP_SPLIT", 1) == 0 || n == 0 || n >= (1ull << 15)) return 1;
+static uint64_t split_factor(const GenDesc &g, uint64_t n, uint64_t T, uint64_t nmax = 1ull << 15) {
+  if (env_int("SLP_SPLIT", 1) == 0 || n == 0 || n >= nmax) return 1;
   const uint64_t bits = (uint64_t)g.n();
   const uint64_t min_wave = std::max<uint64_t>(512, 2 * bits), min_long = std::max<uint64_t>(2048, 8 * bits);
   uint64_t J = 1;
@@ -885,7 +885,7 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int grid = 0;
   int rc;
-  const uint64_t J = split_factor(*g, nstreams, T);
+  const uint64_t J = split_factor(*g, nstreams, T, (uint64_t)env_int("SLP_FUSED_SPLIT_NMAX", 1 << 15));
   if (J > 1) {
     Segments seg;
     rc = make_segments(id, *g, states_in, ld, nstreams, T, J, st, seg);
