@@ -10,9 +10,11 @@ next 1024 outputs (states resident in HBM, advanced in place).  The output
 (8 GiB) is far larger than L2 (126 MB), so no L2 flush is needed between
 steps.  Multi-GPU (torchrun): rank r generates long-jump block r (substreams
 seed * M^(r*2^192 + i*2^128)); there is no data-path collective (weak scaling);
-timing is the max over ranks of CUDA-event time.  ``--impl reference`` times
-the reference's CPU algorithm (oracle/cpu_baseline.py, numpy port, all host
-cores) on rank 0 only.
+timing is the max over ranks of CUDA-event time.  ``--gpus N`` without a
+torchrun environment re-launches itself under ``torch.distributed.run`` with N
+ranks (one per GPU, NCCL).  ``--impl reference`` times the UNMODIFIED reference
+package (``baseline/_ref/slprng``, its own LanedStream set-up + VecStepper /
+apply_vec loop, oracle/ref_baseline.py) on all host cores, rank 0 only.
 """
 
 from __future__ import annotations
@@ -44,7 +46,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--extra", action="store_true", help="also time fused mode and substream init")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the fused-mode (K4) roofline, the config-5 job and the f64 store line")
     return ap.parse_args()
 
 
@@ -146,34 +149,41 @@ def fused_pipes():
         return {}
 
 
-def cpu_baseline(steps_budget_s=20.0):
-    from oracle.cpu_baseline import CpuBaseline
+def golden_checksum(key):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "checksums_big.json")) as f:
+            return json.load(f).get(key, {})
+    except OSError:
+        return {}
 
-    cb = CpuBaseline(GEN, SEED, T)
+
+def cpu_baseline():
+    """The stock reference (baseline/_ref/slprng) on the host cores: config 2's
+    exact partition (2^20 substreams, resident states), one checked warm-up
+    step + 3 timed steps; then the same on one core over 2^15 substreams."""
+    from oracle.ref_baseline import ReferenceArm
+
+    g = golden_checksum(f"c2/{GEN}")
+    arm = ReferenceArm(GEN, SEED, N_STREAMS, T)
     try:
-        lanes = cb.calibrate(min(4.0, steps_budget_s / 4))
-        tot, secs = 0, 0.0
-        reps = 0
-        while secs < steps_budget_s / 2 and reps < 8:
-            n, dt = cb.step(lanes)
-            tot += n
-            secs += dt
-            reps += 1
-        res = {"value": tot / secs, "unit": UNIT, "cores": cb.procs, "kind": "port",
-               "sample": f"{reps} x ({cb.procs} procs x {lanes} substreams x {T} outputs) of config 2, "
-                         "numpy port of LanedStream lane set-up + VecStepper/apply_vec (oracle/cpu_baseline.py), "
-                         "lane set-up included"}
+        _, _, s0, x0 = arm.step(checksum=True)
+        secs = [arm.step()[1] for _ in range(3)]
     finally:
-        cb.close()
-    # the same algorithm on one core (1-core and P-core figures)
-    c1 = CpuBaseline(GEN, SEED, T, procs=1)
+        arm.close()
+    res = {"value": 3 * N_STREAMS * T / sum(secs), "unit": UNIT, "cores": arm.procs, "kind": "reference",
+           "sample": f"3 steps x config 2 (2^20 substreams x {T} outputs, resident states), stock slprng "
+                     f"from baseline/_ref: LanedStream lane set-up once, then apply_vec + VecStepper.step "
+                     f"into a (T, 2^14) buffer per chunk, {arm.procs} worker processes",
+           "matches_reference": bool(g) and (hex(s0), hex(x0)) == (g["sum"], g["xor"]),
+           "setup_s": round(arm.init_wall_s, 3)}
+    one = ReferenceArm(GEN, SEED, 1 << 15, T, procs=1)
     try:
-        lanes1 = c1.calibrate(2.0)
-        n1, dt1 = c1.step(lanes1)
-        res["value_1core"] = n1 / dt1
-        res["sample_1core"] = f"1 proc x {lanes1} substreams x {T} outputs"
+        one.step()
+        n1, dt1 = one.step()
     finally:
-        c1.close()
+        one.close()
+    res["value_1core"] = n1 / dt1
+    res["sample_1core"] = f"1 process x 2^15 substreams x {T} outputs (stock slprng)"
     return res
 
 
@@ -195,6 +205,8 @@ def run_ours(args):
     share = os.environ.get("SLP_BENCH_SHARE_GPU") == "1"
     if share:
         local = 0
+    elif world > torch.cuda.device_count():
+        sys.exit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
     torch.cuda.set_device(local)
     if world > 1:
         if share:
@@ -248,6 +260,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms_local = start.elapsed_time(end)
     ms = max_over_ranks(ms_local)
+
+    # live write-only ceiling of this GPU: a forward-sweep fill of the same
+    # 8 GiB tensor (torch fill_, measurement reference only, outside the timed region)
+    for _ in range(2):
+        out.fill_(1)
+    start.record()
+    for _ in range(10):
+        out.fill_(1)
+    end.record()
+    torch.cuda.synchronize()
+    write_only_gbs = N_STREAMS * T * 8 / (start.elapsed_time(end) / 10 / 1e3) / 1e9
     outputs_per_step = N_STREAMS * T * world
     value = outputs_per_step * args.steps / (ms / 1e3)
 
@@ -264,6 +287,9 @@ def run_ours(args):
                 "alg_bytes_per_unit": "8 B per u64 output + 64 B state read/write per substream per launch",
                 "kernel": "k_fill<xoshiro256**, u64, TMA>", "launch_ms": round(launch_ms, 4),
                 "frac_of_8TBps_spec": round(achieved / 8000.0, 4),
+                "write_only_ceiling_gbs": round(write_only_gbs, 1),
+                "frac_of_write_only_ceiling": round(achieved / write_only_gbs, 4),
+                "write_only_note": "forward-sweep fill_ of the same 8 GiB tensor, measured live on this GPU",
                 "frac_of_write_pattern_ceiling": round(achieved / 6152.0, 4),
                 "write_pattern_ceiling_note": "6152 GB/s = TMA-only store of the same stream-major pattern and "
                                               "geometry (1 KiB row pieces, 7 warps x 1 buffer, no generation), "
@@ -351,8 +377,8 @@ def run_ours(args):
                   "wall_s": round(dt_os, 3)}
 
     extra = {}
-    if args.extra:
-        extra = run_extra(spec, dev, rank)
+    if not args.no_extra:
+        extra = run_extra(spec, dev, rank, world)
 
     if rank == 0:
         cb = None
@@ -371,8 +397,9 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_extra(spec, dev, rank):
-    """Fused mode (K4) on the same substreams + init cost, for DESIGN.md."""
+def run_extra(spec, dev, rank, world):
+    """Fused mode (K4) with its INT roofline on the same substreams, the
+    config-5 job (sharded over the ranks, one collective) and the f64 store."""
     import torch
 
     import paper_1805_01407_b200 as P
@@ -412,24 +439,32 @@ def run_extra(spec, dev, rank):
 
     from paper_1805_01407_b200.multigpu import sharded_checksum
 
-    world = dist.get_world_size() if dist.is_initialized() else 1
-    golden = {}
-    try:
-        with open(os.path.join(ROOT, "tests", "golden", "checksums_big.json")) as f:
-            golden = json.load(f)
-    except OSError:
-        pass
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    # config 5 as a whole job: 2^34 outputs = 8 long-jump blocks x 2^18 substreams
+    # x 2^13, blocks b == rank (mod world), fused exact checksum per GPU, ONE
+    # all_gather of the 64-byte per-rank records (NCCL under torchrun), then
+    # the fold; job time = max over ranks of the barrier-to-result wall time
     c5 = {}
     for name in ("xoshiro512starstar", "xoroshiro1024plusplus"):
         s5 = P.get_spec(name)
-        sharded_checksum(s5, 42, 8, 1 << 18, 1 << 4, rank=rank, world=world, device=dev)  # warm host plans
-        torch.cuda.synchronize()
+        sharded_checksum(s5, 42, 8, 1 << 18, 1 << 4, rank=rank, world=world)  # warm host plans + collective
+        sync_all()
         t0 = time.perf_counter()
-        total, _ = sharded_checksum(s5, 42, 8, 1 << 18, 1 << 13, rank=rank, world=world, device=dev)
+        total, parts = sharded_checksum(s5, 42, 8, 1 << 18, 1 << 13, rank=rank, world=world)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        g = golden.get(f"c5/{name}", {})
-        c5[name] = {"job_s": round(dt, 4), "outputs_per_s": (1 << 34) / dt,
+        if world > 1:
+            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        g = golden_checksum(f"c5/{name}")
+        c5[name] = {"job_s": round(dt, 4), "outputs_per_s": (1 << 34) / dt, "ranks": world,
+                    "blocks_per_rank": [len(range(r, 8, world)) for r in range(world)],
+                    "collective": ("all_gather (" + dist.get_backend() + ")") if world > 1 else "none (1 rank)",
                     "matches_reference": bool(g) and hex(total.sum) == g["sum"] and hex(total.xor) == g["xor"]
                     and hex(total.mant) == g["mant"], "sum": hex(total.sum), "xor": hex(total.xor)}
     res["config5_job"] = c5
@@ -442,47 +477,76 @@ def run_extra(spec, dev, rank):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
     res["store_f64"] = {"outputs_per_s": N_STREAMS * T / (ms / 1e3), "ms_per_step": ms}
-    return {"extra": res}
+    return res
 
 
 # ---------------------------------------------------------------- reference arm
 
 
 def run_reference(args):
+    """The UNMODIFIED reference (baseline/_ref/slprng) on this box's host
+    cores, same metric/config/unit as our arm; rank 0 only under torchrun."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.cpu_baseline import CpuBaseline
+    from oracle.ref_baseline import ReferenceArm
 
-    budget = 120.0
-    per_step = max(0.05, min(3.0, budget / max(1, args.steps + args.warmup)))
-    cb = CpuBaseline(GEN, SEED, T)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    g = golden_checksum(f"c2/{GEN}")
+    arm = ReferenceArm(GEN, SEED, N_STREAMS, T)
     try:
-        lanes = cb.calibrate(per_step)
-        for _ in range(args.warmup):
-            cb.step(lanes)
-        tot, secs = 0, 0.0
-        for _ in range(args.steps):
-            n, dt = cb.step(lanes)
-            tot += n
-            secs += dt
+        # warm-up: the first step from the fresh set-up is config 2 itself -> checked
+        _, _, s0, x0 = arm.step(checksum=True)
+        for _ in range(max(0, args.warmup - 1)):
+            arm.step()
+        secs = [arm.step()[1] for _ in range(args.steps)]
     finally:
-        cb.close()
-    value = tot / secs
-    sample = (f"each step: {cb.procs} procs x {lanes} substreams x {T} outputs of config 2 "
-              "(numpy port of the reference's LanedStream lane set-up + VecStepper/apply_vec)")
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        arm.close()
+    tot = N_STREAMS * T * args.steps
+    value = tot / sum(secs)
+    sample = (f"each step: config 2 whole (2^20 substreams x {T} outputs, states resident and advanced in "
+              f"place), stock slprng from baseline/_ref: LanedStream(lane_len=2^128) set-up once per "
+              f"2^14-lane chunk, then T x (ScramblerSpec.apply_vec, VecStepper.step) into a (T, L) buffer, "
+              f"{arm.procs} worker processes")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(secs) / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded, SplitMix64)", "config": config(world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb.procs, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": arm.procs, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "matches_reference": bool(g) and (hex(s0), hex(x0)) == (g["sum"], g["xor"]),
+            "setup_s": round(arm.init_wall_s, 3),
+            "note": "the GPU arm's world x 2^20 substreams are not replicated here: one host, "
+                    "rank 0 runs the per-GPU workload once"}
     print(json.dumps(line))
+
+
+def relaunch_if_needed(args):
+    """--gpus N > 1 without a torchrun environment: re-exec under
+    torch.distributed.run (one rank per GPU); with one, require WORLD_SIZE == N."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to measure "
+                     f"a different GPU count than requested")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    import subprocess
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
     args = parse()
+    relaunch_if_needed(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -17,7 +17,7 @@ import torch
 
 from .generators import GeneratorSpec
 
-__all__ = ["blocks_for_rank", "gather_checksums", "sharded_checksum", "CHECKSUM_WORDS"]
+__all__ = ["blocks_for_rank", "collective_device", "gather_checksums", "sharded_checksum", "CHECKSUM_WORDS"]
 
 CHECKSUM_WORDS = 8  # words per rank in the all_gather, see _pack()
 
@@ -46,13 +46,27 @@ def _unpack(words, w: int):
                     (words[4] | (words[5] << 64)) if exact else None, words[6], None)
 
 
+def collective_device(group=None, device=None):
+    """Device for the all_gather tensors: ``device`` if given, else the current
+    CUDA device under NCCL (which rejects CPU tensors), else the CPU (gloo)."""
+    import torch.distributed as dist
+
+    if device is not None:
+        return torch.device(device)
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def gather_checksums(c, w: int, group=None, device=None):
-    """all_gather every rank's Checksum (one collective) and fold in rank order."""
+    """all_gather every rank's Checksum (one collective) and fold in rank order.
+    ``device=None`` picks the backend's device (``collective_device``)."""
     import torch.distributed as dist
 
     from .device import Checksum
 
     world = dist.get_world_size(group)
+    device = collective_device(group, device)
     # reinterpret: values >= 2^63 wrap to negative int64, exact round trip
     mine = torch.tensor([x - (1 << 64) if x >= (1 << 63) else x for x in _pack(c)], dtype=torch.int64,
                         device=device)

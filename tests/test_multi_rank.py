@@ -97,3 +97,19 @@ def test_fold_full_c5s_matches_golden(G):
     spec = P.get_spec(g["name"])
     total, _ = sharded_checksum(spec, g["seed"], g["blocks"], g["substreams"], g["T"], compute=oracle_compute)
     assert hex(total.sum) == g["sum"] and hex(total.xor) == g["xor"] and hex(total.mant) == g["mant"]
+
+
+def test_collective_device_follows_backend(monkeypatch):
+    """NCCL rejects CPU tensors: with device=None the all_gather tensor goes to
+    the current CUDA device under nccl and stays on the CPU under gloo."""
+    import torch
+
+    from paper_1805_01407_b200 import multigpu
+
+    monkeypatch.setattr(dist, "get_backend", lambda group=None: "nccl")
+    monkeypatch.setattr(torch.cuda, "current_device", lambda: 3)
+    assert multigpu.collective_device() == torch.device("cuda", 3)
+    assert multigpu.collective_device(device="cpu") == torch.device("cpu")
+    monkeypatch.setattr(dist, "get_backend", lambda group=None: "gloo")
+    assert multigpu.collective_device() == torch.device("cpu")
+    assert multigpu.collective_device(device="cuda:1") == torch.device("cuda", 1)
