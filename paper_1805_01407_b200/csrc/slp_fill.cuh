@@ -70,6 +70,7 @@ __host__ __device__ constexpr FillCfg fill_cfg_at(int i) {
     case 2: return FillCfg{8, 1, 16, 128};
     case 3: return FillCfg{4, 2, 0, 32};  // 512 B rows, two buffers
     case 4: return FillCfg{4, 2, 0, 64};
+    case 5: return FillCfg{4, 1, 16, 32};  // 512 B rows, one buffer (A/B builds only)
     default: return FillCfg{8, 1, 16, 32};  // 0: 1 KiB rows, one buffer
   }
 }
