@@ -517,6 +517,9 @@ def run_reference(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "matches_reference": bool(g) and (hex(s0), hex(x0)) == (g["sum"], g["xor"]),
             "setup_s": round(arm.init_wall_s, 3),
+            # the same step if the stock lane set-up (Generator.jump + LanedStream)
+            # were redone every step instead of once (states resident)
+            "value_setup_each_step": N_STREAMS * T / (arm.init_wall_s + sum(secs) / args.steps),
             "note": "the GPU arm's world x 2^20 substreams are not replicated here: one host, "
                     "rank 0 runs the per-GPU workload once"}
     print(json.dumps(line))

@@ -88,6 +88,18 @@ int slp_num_generators(void);
 int slp_generator_id(const char *name);
 int slp_generator_info(int id, slp_gen_info *out);
 
+/* Registers an arbitrary generator (custom_spec, generators.py:127-135) and
+ * returns an id >= SLP_CUSTOM_ID0 (1024) usable with every entry point below
+ * (or the registry id when the parameters equal a registry generator's).
+ * Fields used: family, k, w, a, b, c, scrambler, word_i, word_j, S, R, T,
+ * name; validation follows EngineKind / _check_params (engines.py:56-97) and
+ * ScramblerSpec.validate (scramblers.py:68-82).  The host algebra accepts
+ * every valid engine; the device kernels (run-time parameter instances)
+ * cover xoroshiro 2x64, 16x64, 2x32, xoshiro 4x64, 8x64, 4x32, 8x32 and
+ * xorshift 2x64, 2x32 -- other shapes return SLP_ERR_UNSUPPORTED from the
+ * device entry points.  Registration is idempotent and thread-safe. */
+int slp_register_generator(const slp_gen_info *spec);
+
 /* ---- host GF(2) algebra (setup; not per output) ------------------------- */
 /* characteristic polynomial of the engine step matrix, bit i = coeff of x^i,
  * little-endian words; replaces engine_char_poly (generators.py:387-394,

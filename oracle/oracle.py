@@ -56,6 +56,27 @@ SPECS = {
 }
 
 
+def _load_custom():
+    """Engines built with the reference's custom_spec (generators.py:127-135):
+    specs and char polys from tests/golden/custom.json (make_golden_custom.py,
+    produced by the reference)."""
+    path = os.path.join(_GOLDEN, "custom.json")
+    if not os.path.exists(path):
+        return {}
+    with open(path) as f:
+        data = json.load(f)
+    polys = {}
+    for name, d in data.items():
+        sc = d["scrambler"]
+        SPECS[name] = (d["family"], d["k"], d["w"], (d["a"], d["b"], d["c"]), sc["kind"], sc.get("word_i", 0),
+                       sc.get("word_j"), sc.get("S"), sc.get("R"), sc.get("T"))
+        polys[f"{d['family']}-{d['k']}-{d['w']}-{d['a']}-{d['b']}-{d['c']}"] = int(d["char_poly"], 16)
+    return polys
+
+
+_CUSTOM_POLYS = _load_custom()
+
+
 def engine_key(name):
     fam, k, w, (a, b, c), *_ = SPECS[name]
     return f"{fam}-{k}-{w}-{a}-{b}-{c}"
@@ -168,7 +189,10 @@ def char_poly(name) -> int:
     if _golden_engines is None:
         with open(os.path.join(_GOLDEN, "engines.json")) as f:
             _golden_engines = json.load(f)
-    return int(_golden_engines[engine_key(name)]["char_poly"], 16)
+    key = engine_key(name)
+    if key in _golden_engines:
+        return int(_golden_engines[key]["char_poly"], 16)
+    return _CUSTOM_POLYS[key]
 
 
 def _clmul(a, b):

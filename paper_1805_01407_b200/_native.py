@@ -67,6 +67,7 @@ SIGNATURES = {
     "slp_num_generators": (ctypes.c_int, []),
     "slp_generator_id": (ctypes.c_int, [ctypes.c_char_p]),
     "slp_generator_info": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(GenInfo)]),
+    "slp_register_generator": (ctypes.c_int, [ctypes.POINTER(GenInfo)]),
     "slp_char_poly": (ctypes.c_int, [ctypes.c_int, u64p, ctypes.c_int]),
     "slp_jump_poly": (ctypes.c_int, [ctypes.c_int, u64p, ctypes.c_int, u64p, ctypes.c_int]),
     "slp_host_jump": (ctypes.c_int, [ctypes.c_int, u64p, ctypes.c_int, u64p]),

@@ -24,11 +24,18 @@ SLP_PART_DECL(2)
 SLP_PART_DECL(3)
 SLP_PART_DECL(4)
 SLP_PART_DECL(5)
+#define SLP_RT_PART_DECL(P) extern const ::slp::GenOps slp_ops_rt_##P[SLP_NUM_RT_SHAPES];
+SLP_RT_PART_DECL(0)
+SLP_RT_PART_DECL(1)
+SLP_RT_PART_DECL(2)
 
 namespace slp {
 
+// kernel dispatch: registry ids -> their compile-time instances; registered
+// custom generators -> the run-time parameter instance of their engine shape
 const GenOps *gen_ops(int id) {
   static GenOps table[SLP_NUM_GENERATORS];
+  static GenOps rt[SLP_NUM_RT_SHAPES];
   static std::once_flag once;
   std::call_once(once, [] {
     const GenOps *parts[] = {slp_ops_part_0, slp_ops_part_1, slp_ops_part_2,
@@ -36,9 +43,36 @@ const GenOps *gen_ops(int id) {
     for (int i = 0; i < SLP_NUM_GENERATORS; ++i)
       for (const GenOps *p : parts)
         if (p[i].fill) table[i] = p[i];
+    const GenOps *rparts[] = {slp_ops_rt_0, slp_ops_rt_1, slp_ops_rt_2};
+    for (int i = 0; i < SLP_NUM_RT_SHAPES; ++i)
+      for (const GenOps *p : rparts)
+        if (p[i].fill) rt[i] = p[i];
   });
+  if (id >= SLP_CUSTOM_ID0) {
+    const GenDesc *g = gen_desc(id);
+    if (!g) return nullptr;
+    const int sh = rt_shape(g->family, g->k, g->w);
+    return sh >= 0 && rt[sh].fill ? &rt[sh] : nullptr;
+  }
   if (id < 0 || id >= SLP_NUM_GENERATORS || !table[id].fill) return nullptr;
   return &table[id];
+}
+
+// run-time parameters of a generator for the GenR<> instances
+GenRt gen_rt(int id) {
+  GenRt r{};
+  const GenDesc *g = gen_desc(id);
+  if (!g) return r;
+  r.a = (uint32_t)g->a;
+  r.b = (uint32_t)g->b;
+  r.c = (uint32_t)g->c;
+  r.sc = g->scrambler;
+  r.wi = g->word_i;
+  r.wj = g->word_j;
+  r.R = (uint32_t)g->R;
+  r.S = g->S;
+  r.T = g->T;
+  return r;
 }
 
 int current_device() {
@@ -337,6 +371,7 @@ static int build_jump_tables(int id, const uint64_t *d_polys, uint64_t first_pol
     for (int i = 0; i < g.n() / 64; ++i) base.w[i] = host_poly[i];
   for (uint64_t i = 0; i < count && rc == SLP_OK; ++i) {
     JumpParams p{};
+    p.rt = gen_rt(id);
     p.src = d_ident;
     p.ld_src = nb;
     p.dst = d_rows;
@@ -465,6 +500,7 @@ static int plan_rounds(const InitPlan &plan, int id, const GenOps *ops, int dev,
     }
     if (L.uniform && tabs && tabs->tables && use_jump_tables(L.count * nblocks)) {
       TableJumpParams tp{};
+      tp.rt = gen_rt(id);
       tp.src = states;
       tp.ld_src = ld;
       tp.dst = states;
@@ -481,6 +517,7 @@ static int plan_rounds(const InitPlan &plan, int id, const GenOps *ops, int dev,
       continue;
     }
     JumpParams p{};
+    p.rt = gen_rt(id);
     p.src = states;
     p.ld_src = ld;
     p.dst = states;
@@ -537,6 +574,7 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
     for (uint64_t b = 0; b < nb; ++b)
       for (int j = 0; j < g->k; ++j) base.w[b * g->k + j] = base_flat[(b0 + b) * g->k + j];
     JumpParams p{};
+    p.rt = gen_rt(id);
     p.src = nullptr;
     p.dst = static_cast<uint8_t *>(states) + b0 * n * esize;
     p.ld_dst = ld;
@@ -588,6 +626,7 @@ int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, co
     const uint64_t nb = n - b0 < 65535 ? n - b0 : 65535;
     void *seg = static_cast<uint8_t *>(seg_states) + b0 * J * esize;
     JumpParams p{};
+    p.rt = gen_rt(id);
     p.src = static_cast<const uint8_t *>(states) + b0 * esize;
     p.ld_src = ld;
     p.dst = seg;
@@ -636,6 +675,7 @@ int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *sr
     if (poly[i]) used = i + 1;
   }
   JumpParams p{};
+  p.rt = gen_rt(id);
   p.src = src;
   p.ld_src = ld_src;
   p.dst = dst;
@@ -661,6 +701,7 @@ int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *sr
     if (rc != SLP_OK) return rc;
     if (table) {
       TableJumpParams tp{};
+      tp.rt = gen_rt(id);
       tp.src = src;
       tp.ld_src = ld_src;
       tp.dst = dst;
@@ -775,6 +816,7 @@ int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint6
   if (layout == SLP_POSITION_MAJOR && ld_out < nstreams) return SLP_ERR_INVALID;
   if (nstreams >= (1ull << 40)) return SLP_ERR_INVALID;
   FillParams p{};
+  p.rt = gen_rt(id);
   p.sin = states_in;
   p.sout = states_out;
   p.ld = ld;
@@ -824,6 +866,7 @@ int slp_fill_checksum(int id, const void *states_in, void *states_out, uint64_t 
   if (nstreams > 0 && T > 0) {
     if (!states_in || !out || ld < nstreams || ld_out < T) return SLP_ERR_INVALID;
     FillParams p{};
+    p.rt = gen_rt(id);
     p.sin = states_in;
     p.sout = states_out;
     p.ld = ld;
@@ -874,6 +917,7 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
   if (!states_in || !result || !workspace || ld < nstreams || !(flags & (SLP_FUSE_INT | SLP_FUSE_F64 | SLP_FUSE_EXACT)))
     return SLP_ERR_INVALID;
   FusedParams p{};
+  p.rt = gen_rt(id);
   p.sin = states_in;
   p.sout = states_out;
   p.ld = ld;
@@ -918,6 +962,7 @@ int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, ui
   if (total > nthreads * tseg || (nthreads && total <= (nthreads - 1) * tseg)) return SLP_ERR_INVALID;
   if (tseg >= (1ull << 32) || warm > 64 || warm0 > 64) return SLP_ERR_INVALID;
   HwdParams p{};
+  p.rt = gen_rt(id);
   p.sin = states;
   p.ld = ld;
   p.nthreads = nthreads;

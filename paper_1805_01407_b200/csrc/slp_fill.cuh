@@ -173,6 +173,7 @@ __device__ __forceinline__ void reduce_checksum_block(uint64_t slo, uint64_t shi
 template <class G, int OK, int MODE, bool CSUM = false, bool SHORT = false, bool TAIL = false>
 __global__ void __launch_bounds__(kFillThreads)
     k_fill(FillParams p, const __grid_constant__ typename FillTmap<MODE>::type tmap) {
+  const G eng = G::load(p.rt);  // run-time parameters (GenR); empty for registry generators
   using word = typename G::word;
   using Cv = Out<OK, word>;
   using bits = typename Cv::bits;
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kFillThreads)
     load_states(u + ustride, nxt);
     if constexpr (MODE == FILL_TMA_G) {  // the lead: this row's outputs before its 16-byte boundary
       for (int t = 0; t < lead; ++t) {
-        const bits x = Cv::conv(G::next_flat(s));
+        const bits x = Cv::conv(eng.next_flat(s));
         if (valid) out[stream * p.ld_out + t] = x;
       }
     }
@@ -313,9 +314,9 @@ __global__ void __launch_bounds__(kFillThreads)
 #pragma unroll
         for (int i = 0; i < EPC; ++i) {
           const int o = (e + i) % K;
-          rr[i] = G::template output_m<MSK>(s, o);
+          rr[i] = eng.template output_m<MSK>(s, o);
           v[i] = Cv::conv(rr[i]);
-          G::template step_m<MSK>(s, o);
+          eng.template step_m<MSK>(s, o);
         }
         if constexpr (CSUM) {
           constexpr uint32_t LOWM = G::w == 64 ? 0x7FFu : 0xFFu;
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(kFillThreads)
     if constexpr (MODE == FILL_POS || MODE == FILL_POS_TMA) {
       // tail positions: each store is one coalesced warp row already
       for (uint64_t t = 0; t < rem; ++t) {
-        const word r = G::next_flat(s);
+        const word r = eng.next_flat(s);
         const bits x = Cv::conv(r);
         if constexpr (CSUM) {
           add128(cs_lo, cs_hi, (uint64_t)r);
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(kFillThreads)
           __syncwarp();
         }
         for (uint32_t t = rb; t < remr; ++t) {
-          const bits x = Cv::conv(G::next_flat(s));
+          const bits x = Cv::conv(eng.next_flat(s));
           if (t < (uint32_t)CH) {
             const uint32_t byte = t * ES;
             const uint32_t addr = tile + taddr(byte >> 7, lane, (byte & 127) >> 4) + (byte & 15);
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(kFillThreads)
           __syncwarp();
         }
         for (uint32_t t = rb; t < (uint32_t)rem; ++t) {
-          const bits x = Cv::conv(G::next_flat(s));
+          const bits x = Cv::conv(eng.next_flat(s));
           const uint32_t byte = t * ES;
           const uint32_t addr = tile + swz(byte >> 7, lane, (byte & 127) >> 4) + (byte & 15);
           if constexpr (ES == 8)
@@ -624,7 +625,7 @@ __global__ void __launch_bounds__(kFillThreads)
       }
       __syncwarp();
       for (uint32_t t = 0; t < (uint32_t)rem; ++t) {
-        const word r = G::next_flat(s);
+        const word r = eng.next_flat(s);
         const bits x = Cv::conv(r);
         if constexpr (CSUM) {
           add128(cs_lo, cs_hi, (uint64_t)r);
@@ -687,6 +688,7 @@ constexpr int kPm2Smem = kFillWarps * 2 * kPm2TileBytes + 1024;
 
 template <class G, int OK>
 __global__ void __launch_bounds__(kFillThreads) k_fill_pm2(FillParams p, const __grid_constant__ CUtensorMap tmap) {
+  const G eng = G::load(p.rt);
   using word = typename G::word;
   using Cv = Out<OK, word>;
   using bits = typename Cv::bits;
@@ -720,10 +722,10 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pm2(FillParams p, const _
 #pragma unroll
       for (int t = 0; t < kPm2Pos; ++t) {
         const int o = t % K;
-        const bits xa = Cv::conv(G::template output_m<MSK>(a, o));
-        G::template step_m<MSK>(a, o);
-        const bits xb = Cv::conv(G::template output_m<MSK>(b, o));
-        G::template step_m<MSK>(b, o);
+        const bits xa = Cv::conv(eng.template output_m<MSK>(a, o));
+        eng.template step_m<MSK>(a, o);
+        const bits xb = Cv::conv(eng.template output_m<MSK>(b, o));
+        eng.template step_m<MSK>(b, o);
         const uint32_t row = tile + t * 256 + lane * 4;
         asm volatile("st.shared.b32 [%0], %1;" ::"r"(row), "r"((uint32_t)xa) : "memory");
         asm volatile("st.shared.b32 [%0], %1;" ::"r"(row + 128), "r"((uint32_t)xb) : "memory");
@@ -737,8 +739,8 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pm2(FillParams p, const _
       ++issued;
     }
     for (uint64_t t = 0; t < rem; ++t) {  // tail positions: coalesced warp rows
-      const bits xa = Cv::conv(G::next_flat(a));
-      const bits xb = Cv::conv(G::next_flat(b));
+      const bits xa = Cv::conv(eng.next_flat(a));
+      const bits xb = Cv::conv(eng.next_flat(b));
       const uint64_t pos = ntiles * kPm2Pos + t;
       if (vA) out[pos * p.ld_out + stA] = xa;
       if (vB) out[pos * p.ld_out + stB] = xb;

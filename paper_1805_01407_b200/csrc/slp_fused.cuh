@@ -21,6 +21,7 @@ template <class G, bool MANT, bool F64>
 #define SLP_FUSED_MINB 1
 #endif
 __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedParams p) {
+  const G eng = G::load(p.rt);
   using word = typename G::word;
   constexpr int K = G::k;
   constexpr int CH = 16;  // multiple of every ring size
@@ -57,10 +58,10 @@ __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedPa
       word xx = 0;
 #pragma unroll
       for (int t = 0; t < CH; t += 2) {
-        const word o0 = G::template output_m<MSK>(s, t % K);
-        G::template step_m<MSK>(s, t % K);
-        const word o1 = G::template output_m<MSK>(s, (t + 1) % K);
-        G::template step_m<MSK>(s, (t + 1) % K);
+        const word o0 = eng.template output_m<MSK>(s, t % K);
+        eng.template step_m<MSK>(s, t % K);
+        const word o1 = eng.template output_m<MSK>(s, (t + 1) % K);
+        eng.template step_m<MSK>(s, (t + 1) % K);
 #if SLP_SUM_POLICY == 2
         // separate even/odd accumulators: one IMAD.WIDE per chain per pair,
         // nothing for ptxas to re-associate into IADD3
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedPa
 #endif
     }
     for (uint64_t t = 0; t < rem; ++t) {
-      const word x = G::next_flat(s);
+      const word x = eng.next_flat(s);
       acc_lo += (uint32_t)x;
       if constexpr (G::w == 64) acc_hi += (uint32_t)((uint64_t)x >> 32);
       sx ^= (uint64_t)x;

@@ -189,6 +189,11 @@ struct Gen {
   static constexpr bool ring = FAM != SLP_FAM_XOSHIRO;
   static constexpr int sc = SC;
   static constexpr int fam = FAM;
+  static constexpr bool runtime = false;
+  // kernels call the generator through an object (`eng.step(...)`) so that
+  // the same code serves GenR<> below, whose parameters are run-time values;
+  // for Gen<> the object is empty and every member is static
+  static __device__ __forceinline__ Gen load(const GenRt &) { return Gen{}; }
 
   // Rotation sites that may run on either pipe (bit set in a mask = FMA form):
   //   bit 0: engine rotation by A (xoroshiro) / by B (xoshiro)
@@ -316,6 +321,133 @@ struct Gen {
 
   // one output + step, registers left in flat order (tails of odd length)
   static __device__ __forceinline__ word next_flat(word (&s)[K]) {
+    const word out = output(s, 0);
+    step(s, 0);
+    if constexpr (ring) {
+      const word first = s[0];
+#pragma unroll
+      for (int j = 0; j + 1 < K; ++j) s[j] = s[j + 1];
+      s[K - 1] = first;
+    }
+    return out;
+  }
+};
+
+// ---- run-time parameter generators (custom_spec engines) ---------------------
+//
+// The reference accepts any engine built with custom_spec
+// (generators.py:127-135) in LanedStream / output_stream / VecStepper
+// (generators.py:426-513, engines.py:276-361).  GenR<FAM, K, W> is one kernel
+// instance per engine SHAPE (family, k, w): shift/rotation amounts,
+// scrambler kind, word indices and multipliers are loaded once per thread
+// from the launch parameters (GenRt) into registers.  Same state layout,
+// ring handling and statement order as Gen<>; rotations and shifts take a
+// register amount (SHF with a variable shift), word selection is a
+// warp-uniform select chain instead of a register index (which would spill
+// the state to local memory).
+template <int FAM, int K, int W>
+struct GenR {
+  static constexpr int id = -1;  // no tuned fill configuration: the default one
+  using word = typename WordOf<W>::type;
+  static constexpr int k = K;
+  static constexpr int w = W;
+  static constexpr int n = K * W;
+  static constexpr int pw = n / 64;
+  static constexpr bool ring = FAM != SLP_FAM_XOSHIRO;
+  static constexpr int fam = FAM;
+  static constexpr bool runtime = true;
+  static_assert(n % 64 == 0, "state size must be a whole number of 64-bit words");
+
+  uint32_t a, b, c, r;
+  int sc, wi, wj;
+  word S, T;
+
+  static __device__ __forceinline__ GenR load(const GenRt &p) {
+    GenR g;
+    g.a = p.a;
+    g.b = p.b;
+    g.c = p.c;
+    g.r = p.R;
+    g.sc = p.sc;
+    g.wi = p.wi;
+    g.wj = p.wj < 0 ? 0 : p.wj;
+    g.S = (word)p.S;
+    g.T = (word)p.T;
+    return g;
+  }
+  static __host__ __device__ constexpr int best_mask(int, int) { return 0; }
+  static __device__ __forceinline__ constexpr int slot(int o, int j) { return ring ? (o + j) % K : j; }
+
+  static __device__ __forceinline__ word rotl(word x, uint32_t s) {
+    if constexpr (W == 32) {
+      return __funnelshift_l(x, x, s);
+    } else {
+      uint32_t l = (uint32_t)x, h = (uint32_t)(x >> 32);
+      if (s & 32) {
+        const uint32_t t = l;
+        l = h;
+        h = t;
+      }
+      return ((uint64_t)__funnelshift_l(l, h, s) << 32) | __funnelshift_l(h, l, s);
+    }
+  }
+  // flat word j at ring offset o; j is a run-time value
+  __device__ __forceinline__ word pick(const word (&s)[K], int o, int j) const {
+    word v = s[slot(o, 0)];
+#pragma unroll
+    for (int i = 1; i < K; ++i) v = j == i ? s[slot(o, i)] : v;
+    return v;
+  }
+
+  template <int M>
+  __device__ __forceinline__ word output_m(const word (&s)[K], int o) const {
+    const word xi = pick(s, o, wi);
+    switch (sc) {
+      case SLP_SC_PLUS: return (word)(xi + pick(s, o, wj));
+      case SLP_SC_STAR: return (word)(xi * S);
+      case SLP_SC_PLUSPLUS: return (word)(rotl((word)(xi + pick(s, o, wj)), r) + xi);
+      case SLP_SC_STARSTAR: return (word)(rotl((word)(xi * S), r) * T);
+      default: return xi;
+    }
+  }
+  template <int M>
+  __device__ __forceinline__ void step_m(word (&s)[K], int o) const {
+    if constexpr (FAM == SLP_FAM_XOROSHIRO) {
+      const int i0 = slot(o, 0), il = slot(o, K - 1);
+      const word x0 = s[i0];
+      const word xl = s[il] ^ x0;
+      s[il] = rotl(x0, a) ^ xl ^ (word)(xl << b);
+      s[i0] = rotl(xl, c);
+    } else if constexpr (FAM == SLP_FAM_XORSHIFT) {
+      const int i0 = slot(o, 0), i1 = slot(o, 1);
+      const word s0 = s[i0], s1 = s[i1];
+      const word t = s0 ^ (word)(s0 << a);
+      s[i0] = t ^ (t >> b) ^ s1 ^ (s1 >> c);
+    } else if constexpr (K == 4) {
+      const word t = (word)(s[1] << a);
+      s[2] ^= s[0];
+      s[3] ^= s[1];
+      s[1] ^= s[2];
+      s[0] ^= s[3];
+      s[2] ^= t;
+      s[3] = rotl(s[3], b);
+    } else {
+      const word t = (word)(s[1] << a);
+      s[2] ^= s[0];
+      s[5] ^= s[1];
+      s[1] ^= s[2];
+      s[7] ^= s[3];
+      s[3] ^= s[4];
+      s[4] ^= s[5];
+      s[0] ^= s[6];
+      s[6] ^= s[7];
+      s[6] ^= t;
+      s[7] = rotl(s[7], b);
+    }
+  }
+  __device__ __forceinline__ word output(const word (&s)[K], int o) const { return output_m<0>(s, o); }
+  __device__ __forceinline__ void step(word (&s)[K], int o) const { step_m<0>(s, o); }
+  __device__ __forceinline__ word next_flat(word (&s)[K]) const {
     const word out = output(s, 0);
     step(s, 0);
     if constexpr (ring) {

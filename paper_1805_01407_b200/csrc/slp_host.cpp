@@ -11,6 +11,7 @@
 //   lane doubling         generators.py:450-459 (here: radix-8 rounds, see init_plan)
 #include <immintrin.h>
 
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -32,16 +33,42 @@ static const GenDesc kGens[SLP_NUM_GENERATORS] = {
 #undef SLP_X
 };
 
+// registered custom generators (custom_spec, generators.py:127-135), ids
+// SLP_CUSTOM_ID0 + i; entries are never removed, so pointers stay valid
+struct CustomGen {
+  GenDesc d;
+  char name[32];
+};
+static std::unique_ptr<CustomGen> g_custom[SLP_MAX_CUSTOM];
+static std::atomic<int> g_ncustom{0};
+static std::mutex g_custom_mu;
+
 const GenDesc *gen_desc(int id) {
-  if (id < 0 || id >= SLP_NUM_GENERATORS) return nullptr;
-  return &kGens[id];
+  if (id >= 0 && id < SLP_NUM_GENERATORS) return &kGens[id];
+  if (id >= SLP_CUSTOM_ID0 && id < SLP_CUSTOM_ID0 + g_ncustom.load(std::memory_order_acquire))
+    return &g_custom[id - SLP_CUSTOM_ID0]->d;
+  return nullptr;
 }
 
+// the smallest registry id with the same engine, else the first registered
+// custom generator with it: plans and jump tables are shared per engine
 int engine_id(int id) {
   const GenDesc *g = gen_desc(id);
+  if (!g) return id;
   for (int i = 0; i < SLP_NUM_GENERATORS; ++i)
     if (kGens[i].same_engine(*g)) return i;
+  const int n = g_ncustom.load(std::memory_order_acquire);
+  for (int i = 0; i < n; ++i)
+    if (g_custom[i]->d.same_engine(*g)) return SLP_CUSTOM_ID0 + i;
   return id;
+}
+
+int rt_shape(int family, int k, int w) {
+#define SLP_SHAPE_X(i, fam, kk, ww) \
+  if (family == (fam) && k == (kk) && w == (ww)) return i;
+  SLP_RT_SHAPES(SLP_SHAPE_X)
+#undef SLP_SHAPE_X
+  return -1;
 }
 
 static thread_local std::string t_last_error;
@@ -703,6 +730,57 @@ static int custom_desc(int family, int k, int w, int a, int b, int c, GenDesc *g
   if (!(0 < a && a < w) || !(0 < b && b < w) || (needs_c && !(0 < c && c < w))) return SLP_ERR_INVALID;
   *g = GenDesc{-1, "custom", family, k, w, a, b, needs_c ? c : 0, SLP_SC_NONE, 0, -1, 0, 0, 0};
   return SLP_OK;
+}
+
+static bool scrambler_ok(const slp_gen_info &s, int k, int w) {
+  // ScramblerSpec.validate (scramblers.py:68-82)
+  if (s.scrambler < SLP_SC_NONE || s.scrambler > SLP_SC_STARSTAR) return false;
+  if (s.word_i < 0 || s.word_i >= k) return false;
+  if ((s.scrambler == SLP_SC_PLUS || s.scrambler == SLP_SC_PLUSPLUS) && (s.word_j < 0 || s.word_j >= k)) return false;
+  if ((s.scrambler == SLP_SC_STAR || s.scrambler == SLP_SC_STARSTAR) && (s.S % 2 == 0)) return false;
+  if ((s.scrambler == SLP_SC_PLUSPLUS || s.scrambler == SLP_SC_STARSTAR) && !(0 < s.R && s.R < w)) return false;
+  if (s.scrambler == SLP_SC_STARSTAR && s.T % 2 == 0) return false;
+  return true;
+}
+
+int slp_register_generator(const slp_gen_info *spec) {
+  if (!spec) return SLP_ERR_INVALID;
+  GenDesc g;
+  int rc = custom_desc(spec->family, spec->k, spec->w, spec->a, spec->b, spec->c, &g);
+  if (rc != SLP_OK) return rc;
+  if (!scrambler_ok(*spec, g.k, g.w)) return SLP_ERR_INVALID;
+  const uint64_t wmask = g.w == 64 ? ~0ull : ((1ull << g.w) - 1);
+  g.scrambler = spec->scrambler;
+  g.word_i = spec->word_i;
+  const bool uses_j = g.scrambler == SLP_SC_PLUS || g.scrambler == SLP_SC_PLUSPLUS;
+  g.word_j = uses_j ? spec->word_j : -1;
+  const bool uses_s = g.scrambler == SLP_SC_STAR || g.scrambler == SLP_SC_STARSTAR;
+  g.S = uses_s ? spec->S & wmask : 0;  // (x * S) mod 2^w only depends on S mod 2^w
+  g.R = (g.scrambler == SLP_SC_PLUSPLUS || g.scrambler == SLP_SC_STARSTAR) ? spec->R : 0;
+  g.T = g.scrambler == SLP_SC_STARSTAR ? spec->T & wmask : 0;
+  auto same = [&](const GenDesc &o) {
+    return o.same_engine(g) && o.scrambler == g.scrambler && o.word_i == g.word_i && o.word_j == g.word_j &&
+           o.S == g.S && o.R == g.R && o.T == g.T;
+  };
+  for (int i = 0; i < SLP_NUM_GENERATORS; ++i)
+    if (same(kGens[i])) return i;  // identical to a registry generator: same kernels
+  std::lock_guard<std::mutex> lk(g_custom_mu);
+  const int n = g_ncustom.load(std::memory_order_relaxed);
+  for (int i = 0; i < n; ++i)
+    if (same(g_custom[i]->d)) return SLP_CUSTOM_ID0 + i;
+  if (n >= SLP_MAX_CUSTOM) {
+    set_last_error("too many registered custom generators");
+    return SLP_ERR_BUFFER;
+  }
+  auto c = std::make_unique<CustomGen>();
+  c->d = g;
+  c->d.id = SLP_CUSTOM_ID0 + n;
+  std::memset(c->name, 0, sizeof c->name);
+  std::strncpy(c->name, spec->name[0] ? spec->name : "custom", sizeof(c->name) - 1);
+  c->d.name = c->name;
+  g_custom[n] = std::move(c);
+  g_ncustom.store(n + 1, std::memory_order_release);
+  return SLP_CUSTOM_ID0 + n;
 }
 
 int slp_engine_char_poly(int family, int k, int w, int a, int b, int c, uint64_t *poly, int poly_words) {

@@ -34,6 +34,7 @@ constexpr uint32_t kHwdRecip = 0x55555556u;  // ceil(2^32 / 3), hwd.py:44
 template <class G, bool TRANS, bool SPLIT, bool GLOBAL, bool SLICED = false>
 __device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, uint32_t *cells,
                                                 uint32_t cell_lo = 0) {
+  const G eng = G::load(p.rt);
   using word = typename G::word;
   constexpr int K = G::k;
   constexpr int TW = SPLIT ? 32 : G::w;  // test-value width
@@ -82,7 +83,7 @@ __device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, 
   bool pending = false;
   uint64_t pend = 0;
   while (warm > 0) {
-    const word x = G::next_flat(s);
+    const word x = eng.next_flat(s);
     if constexpr (SPLIT) {
       consume((uint64_t)x & 0xFFFFFFFFull, false);
       if (--warm > 0) {
@@ -107,8 +108,8 @@ __device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, 
   for (uint32_t c = cnt / (CH * VPW); c > 0; --c) {
 #pragma unroll
     for (int t = 0; t < CH; ++t) {
-      const word x = G::output(s, t % K);
-      G::step(s, t % K);
+      const word x = eng.output(s, t % K);
+      eng.step(s, t % K);
       if constexpr (SPLIT) {
         consume((uint64_t)x & 0xFFFFFFFFull, true);
         consume((uint64_t)x >> 32, true);
@@ -120,7 +121,7 @@ __device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, 
   cnt %= CH * VPW;
   // phase C: tail
   while (cnt > 0) {
-    const word x = G::next_flat(s);
+    const word x = eng.next_flat(s);
     if constexpr (SPLIT) {
       consume((uint64_t)x & 0xFFFFFFFFull, true);
       if (--cnt > 0) {

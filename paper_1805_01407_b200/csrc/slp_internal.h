@@ -34,6 +34,7 @@ struct GenDesc {
 
 const GenDesc *gen_desc(int id);  // nullptr if out of range
 int engine_id(int id);            // smallest generator id with the same engine
+int rt_shape(int family, int k, int w);  // SLP_RT_SHAPES index of an engine shape, or -1
 
 // ---- GF(2) polynomials: little-endian u64 words, bit i = coeff of x^i -----
 using Poly = std::vector<uint64_t>;

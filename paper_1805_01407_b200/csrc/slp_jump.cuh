@@ -17,6 +17,7 @@ constexpr int kJumpThreads = 128;
 
 template <class G, bool UNIFORM>
 __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __grid_constant__ BaseStates base) {
+  const G eng = G::load(p.rt);
   using word = typename G::word;
   constexpr int K = G::k;
   uint64_t t = (uint64_t)blockIdx.x * kJumpThreads + threadIdx.x;
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __gri
 #pragma unroll
           for (int j = 0; j < K; ++j) acc[j] ^= cur[G::slot(o, j)] & msk;
         }
-        G::step(cur, o);
+        eng.step(cur, o);
       }
     }
   }

@@ -8,6 +8,16 @@
 
 namespace slp {
 
+// Run-time generator parameters (custom_spec engines, generators.py:127-135):
+// read by the GenR<> kernel instances (slp_gen.cuh), ignored by the
+// registry instances, whose parameters are template constants.
+struct GenRt {
+  uint32_t a, b, c;     // engine shift/rotation amounts (engines.py:100-140)
+  int32_t sc, wi, wj;   // scrambler kind (SLP_SC_*) and flat word indices (wj < 0: unused)
+  uint32_t R;           // scrambler rotation (++ and **)
+  uint64_t S, T;        // scrambler multipliers (* and **)
+};
+
 struct FillParams {
   const void *sin;   // SoA states [k][ld]
   void *sout;        // may alias sin; nullptr = no write-back
@@ -19,6 +29,7 @@ struct FillParams {
   uint64_t nunits;   // filled by the launcher
   void *partials;           // store+checksum mode: slp_checksum[grid]
   size_t workspace_bytes;
+  GenRt rt;                // run-time generator parameters (custom engines)
 };
 
 struct FusedParams {
@@ -31,6 +42,7 @@ struct FusedParams {
   size_t workspace_bytes;  // bytes available at partials
   uint64_t nunits;
   uint32_t one;            // = 1, opaque to ptxas (keeps accumulations on IMAD)
+  GenRt rt;                // run-time generator parameters (custom engines)
 };
 
 struct JumpParams {
@@ -48,6 +60,7 @@ struct JumpParams {
   uint64_t src_batch_stride;  // source states per batch (0: batch_stride)
   uint64_t fold;              // > 0: batches folded into t (batch t / fold, index t % fold), grid.y = 1
   int pw_used;            // polynomial words actually used (0 = all); trims the loop for low-degree polys
+  GenRt rt;                // run-time generator parameters (custom engines)
 };
 
 // table-driven uniform jump (kernel K1t): dst[dst_off + t] = src[src_off + t % m]
@@ -61,6 +74,7 @@ struct TableJumpParams {
   uint64_t table0;
   uint64_t count, m;
   uint64_t src_off, dst_off, batch_stride;
+  GenRt rt;                // run-time generator parameters (custom engines)
 };
 
 // fill tile geometry (kernel K2): each warp emits tiles of 32 substreams x
@@ -96,6 +110,7 @@ struct HwdParams {
                              // [y * slice_cells, (y + 1) * slice_cells) (gridDim.y slices)
   unsigned long long *g_counts, *g_sums;  // 3^k each, accumulated
   unsigned long long *overflow_ctas;      // nullable: CTAs that fell back to the exact recount
+  GenRt rt;                // run-time generator parameters (custom engines)
 };
 
 struct GenOps {

@@ -57,3 +57,24 @@
 
 #define SLP_NUM_GENERATORS 27
 #define SLP_NUM_PRODUCTION 25
+
+// Engine shapes (family, k, w) with run-time parameter kernel instances
+// (GenR<>, slp_gen.cuh) for custom_spec engines (generators.py:127-135):
+// the registry's engine shapes with any parameters, plus the 32-bit
+// xorshift and 8-word xoshiro.  X(shape index, family, k, w)
+// clang-format off
+#define SLP_RT_SHAPES(X) \
+  X(0, SLP_FAM_XOROSHIRO,  2, 64) \
+  X(1, SLP_FAM_XOROSHIRO, 16, 64) \
+  X(2, SLP_FAM_XOSHIRO,    4, 64) \
+  X(3, SLP_FAM_XOSHIRO,    8, 64) \
+  X(4, SLP_FAM_XORSHIFT,   2, 64) \
+  X(5, SLP_FAM_XOROSHIRO,  2, 32) \
+  X(6, SLP_FAM_XOSHIRO,    4, 32) \
+  X(7, SLP_FAM_XOSHIRO,    8, 32) \
+  X(8, SLP_FAM_XORSHIFT,   2, 32)
+// clang-format on
+#define SLP_NUM_RT_SHAPES 9
+// ids of registered custom generators (slp_register_generator) start here
+#define SLP_CUSTOM_ID0 1024
+#define SLP_MAX_CUSTOM 4096

@@ -416,14 +416,19 @@ class VecStepper:
     steps (kernel K1)."""
 
     def __init__(self, kind, params):
+        from .engines import check_params
         from .generators import _TABLE
+        from .scramblers import ScramblerSpec
 
+        if kind.w not in (32, 64):  # engines.py:291-292
+            raise ValueError("vector stepping supports w in {32, 64} only")
+        check_params(kind, params)
         match = [s for s in _TABLE if s.kind == kind and s.params == params]
-        if not match:
-            raise ValueError("the device VecStepper supports the registry engines only")
+        # any other engine (custom_spec) runs on the run-time parameter kernels
+        self.spec = match[0] if match else GeneratorSpec(f"{kind.family}{kind.n}-vec", kind, params,
+                                                           ScramblerSpec("none", 0))
         self.kind = kind
         self.params = params
-        self.spec = match[0]
         self.off = 0
         self._scratch = None
 

@@ -16,7 +16,17 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 __all__ = ["EngineKind", "EngineParams", "rotl", "step", "state_to_bits", "bits_to_words",
-           "check_params", "FAMILIES"]
+           "check_params", "FAMILIES", "VecStepper"]
+
+
+def __getattr__(name):
+    # engines.VecStepper (engines.py:276-361): the device-backed lane stepper
+    # of device.py, imported lazily (device.py imports torch and this module)
+    if name == "VecStepper":
+        from .device import VecStepper
+
+        return VecStepper
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
 
 FAMILIES = ("xoroshiro", "xoshiro", "xorshift")
 FAMILY_CODE = {"xoroshiro": 0, "xoshiro": 1, "xorshift": 2}
