@@ -216,6 +216,10 @@ int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, ui
                   uint64_t *counts, uint64_t *sums, uint64_t *overflow_ctas, void *stream);
 
 /* ---- misc ---------------------------------------------------------------- */
+/* Bytes held by the device-side cache of `device` (init-plan polynomials and
+ * K1t jump tables): a bounded LRU of SLP_DEVICE_CACHE_MB (default 1024) MiB
+ * per device, built and freed stream-ordered (no host synchronisation). */
+size_t slp_device_cache_bytes(int device);
 const char *slp_status_str(int status);
 /* last CUDA error string seen by this thread ("" if none) */
 const char *slp_last_error(void);

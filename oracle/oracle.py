@@ -56,6 +56,9 @@ SPECS = {
 }
 
 
+REGISTRY_NAMES = list(SPECS)  # the reference registry; custom engines are appended below
+
+
 def _load_custom():
     """Engines built with the reference's custom_spec (generators.py:127-135):
     specs and char polys from tests/golden/custom.json (make_golden_custom.py,

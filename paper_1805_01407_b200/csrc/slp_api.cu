@@ -304,42 +304,132 @@ __global__ void k_segment_ends(const W *seg, uint64_t n, uint64_t J, int k, W *o
 }
 }  // namespace dev
 
-// device copies of the init-plan polynomials, per (plan, device)
-static std::mutex g_dev_mu;
-static std::map<std::pair<const InitPlan *, int>, void *> g_dev_polys;
+// ---- device-side caches ----------------------------------------------------
+// Init-plan polynomials and K1t jump tables live in one bounded LRU per
+// device (SLP_DEVICE_CACHE_MB, default 1024).  Nothing here synchronises the
+// host, so a fill stays asynchronous (and capturable) even when it needs a new
+// plan: an entry is built stream-ordered on the caller's stream
+// (cudaMallocAsync + copies + kernels) and published with a `ready` event
+// that every later user waits on (cudaStreamWaitEvent) before its launches.
+// Every use records a per-stream `last use` event; evicting an entry orders
+// its cudaFreeAsync after those events, so memory is never freed under a
+// kernel that still reads it.  Entries are pinned while a call holds them.
+namespace {
+struct DevEntry {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+  uint64_t tick = 0;
+  int pins = 0;
+  cudaEvent_t ready = nullptr;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
+  uint64_t first_poly = 0, count = 0;  // table sets: polynomials [first, first + count) of the plan
+};
+enum { CACHE_PLAN_POLYS = 0, CACHE_PLAN_TABLES = 1, CACHE_POLY_TABLE = 2 };
+using DevKey = std::tuple<int, int, std::vector<uint64_t>>;  // (kind, device, key words)
 
-static int plan_polys_on_device(const InitPlan &plan, int dev, const uint64_t **out) {
-  std::lock_guard<std::mutex> lk(g_dev_mu);
-  auto key = std::make_pair(&plan, dev);
-  auto it = g_dev_polys.find(key);
-  if (it != g_dev_polys.end()) {
-    *out = static_cast<const uint64_t *>(it->second);
-    return SLP_OK;
+std::mutex g_cache_mu;
+std::map<DevKey, std::unique_ptr<DevEntry>> g_cache;
+std::map<int, size_t> g_cache_bytes;
+uint64_t g_cache_tick = 0;
+
+size_t cache_budget() {
+  static size_t b = (size_t)std::max(64, env_int("SLP_DEVICE_CACHE_MB", 1024)) << 20;
+  return b;
+}
+
+// with g_cache_mu held: the entry, pinned and waited on by `st`, or nullptr
+DevEntry *cache_find(const DevKey &key, cudaStream_t st) {
+  auto it = g_cache.find(key);
+  if (it == g_cache.end()) return nullptr;
+  DevEntry *e = it->second.get();
+  e->tick = ++g_cache_tick;
+  ++e->pins;
+  if (e->ready) cudaStreamWaitEvent(st, e->ready, 0);
+  return e;
+}
+
+void release_entry(DevEntry &e, cudaStream_t st) {  // frees after every recorded use (stream-ordered)
+  for (auto &u : e.uses) {
+    cudaStreamWaitEvent(st, u.second, 0);
+    cudaEventDestroy(u.second);
   }
-  void *d = nullptr;
-  const size_t bytes = plan.polys.size() * sizeof(uint64_t);
-  if (cudaMalloc(&d, bytes) != cudaSuccess) return cuda_fail("cudaMalloc(init polys)");
-  if (cudaMemcpy(d, plan.polys.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
-    cudaFree(d);
-    return cuda_fail("cudaMemcpy(init polys)");
+  if (e.ready) {
+    cudaStreamWaitEvent(st, e.ready, 0);
+    cudaEventDestroy(e.ready);
   }
-  g_dev_polys[key] = d;
-  *out = static_cast<const uint64_t *>(d);
+  if (e.ptr) cudaFreeAsync(e.ptr, st);
+}
+
+// with g_cache_mu held: publish a freshly built entry (pinned), evicting
+// least-recently-used unpinned entries of the device beyond the budget
+DevEntry *cache_insert(const DevKey &key, std::unique_ptr<DevEntry> e, cudaStream_t st) {
+  const int dev = std::get<1>(key);
+  e->tick = ++g_cache_tick;
+  e->pins = 1;
+  if (cudaEventCreateWithFlags(&e->ready, cudaEventDisableTiming) == cudaSuccess) cudaEventRecord(e->ready, st);
+  g_cache_bytes[dev] += e->bytes;
+  DevEntry *raw = e.get();
+  g_cache[key] = std::move(e);
+  while (g_cache_bytes[dev] > cache_budget()) {
+    auto lru = g_cache.end();
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+      if (std::get<1>(it->first) == dev && it->second->pins == 0 &&
+          (lru == g_cache.end() || it->second->tick < lru->second->tick))
+        lru = it;
+    if (lru == g_cache.end()) break;  // everything else is in use: stay over budget for now
+    g_cache_bytes[dev] -= lru->second->bytes;
+    release_entry(*lru->second, st);
+    g_cache.erase(lru);
+  }
+  return raw;
+}
+
+// the caller's launches on `st` that read the entry are enqueued: record the
+// last use on this stream and unpin
+void cache_unpin(DevEntry *e, cudaStream_t st) {
+  if (!e) return;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  cudaEvent_t ev = nullptr;
+  for (auto &u : e->uses)
+    if (u.first == st) ev = u.second;
+  if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) e->uses.emplace_back(st, ev);
+  if (ev) cudaEventRecord(ev, st);
+  --e->pins;
+}
+
+// unpins on scope exit
+struct Pinned {
+  DevEntry *e = nullptr;
+  cudaStream_t st = nullptr;
+  Pinned() = default;
+  Pinned(const Pinned &) = delete;
+  Pinned &operator=(const Pinned &) = delete;
+  ~Pinned() { cache_unpin(e, st); }
+};
+}  // namespace
+
+// device copy of a plan's polynomials (H2D on `st`, stream-ordered)
+static int plan_polys_on_device(const InitPlan &plan, int dev, cudaStream_t st, Pinned &pin) {
+  const DevKey key{CACHE_PLAN_POLYS, dev, {plan.uid}};
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  pin.st = st;
+  if ((pin.e = cache_find(key, st))) return SLP_OK;
+  auto e = std::make_unique<DevEntry>();
+  e->bytes = plan.polys.size() * sizeof(uint64_t);
+  if (cudaMallocAsync(&e->ptr, e->bytes, st) != cudaSuccess) return cuda_fail("cudaMallocAsync(init polys)");
+  if (cudaMemcpyAsync(e->ptr, plan.polys.data(), e->bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    cudaFreeAsync(e->ptr, st);
+    return cuda_fail("cudaMemcpyAsync(init polys)");
+  }
+  pin.e = cache_insert(key, std::move(e), st);
   return SLP_OK;
 }
 
-// K1t jump tables of an init plan's round polynomials, per (plan, device):
-// row i of each jump matrix is unit vector i jumped by K1 (one launch over
-// the n unit vectors), then expanded into four-Russians tables on the device
-struct DevTables {
-  uint32_t *tables = nullptr;
-  uint64_t first_poly = 0, count = 0;
-};
-static std::map<std::pair<const InitPlan *, int>, DevTables> g_dev_tables;
-
-// builds `count` K1t tables on `st` (synchronised before returning): table i
-// from polynomial i of the device array `d_polys` (or, when d_polys is null,
-// from the single host polynomial `host_poly` passed as a kernel parameter)
+// builds `count` K1t tables on `st` (stream-ordered, no host synchronisation):
+// table i from polynomial i of the device array `d_polys` (or, when d_polys
+// is null, from the single host polynomial `host_poly` passed as a kernel
+// parameter).  Row r of a jump matrix is unit vector r jumped by K1 (one
+// launch over the n unit vectors), then expanded into four-Russians tables.
 static int build_jump_tables(int id, const uint64_t *d_polys, uint64_t first_poly, const uint64_t *host_poly,
                              uint64_t count, cudaStream_t st, uint32_t **out) {
   const GenDesc &g = *gen_desc(id);
@@ -355,13 +445,14 @@ static int build_jump_tables(int id, const uint64_t *d_polys, uint64_t first_pol
   const uint64_t tw = ops->table_words();
   void *d_ident = nullptr, *d_rows = nullptr;
   uint32_t *tables = nullptr;
-  if (cudaMalloc(&d_ident, ident.size()) != cudaSuccess) return cuda_fail("cudaMalloc(jump tables)");
-  if (cudaMalloc(&d_rows, ident.size()) != cudaSuccess ||
-      cudaMalloc(reinterpret_cast<void **>(&tables), count * tw * sizeof(uint32_t)) != cudaSuccess) {
-    cudaFree(d_ident);
-    cudaFree(d_rows);
-    return cuda_fail("cudaMalloc(jump tables)");
+  if (cudaMallocAsync(&d_ident, ident.size(), st) != cudaSuccess) return cuda_fail("cudaMallocAsync(jump tables)");
+  if (cudaMallocAsync(&d_rows, ident.size(), st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void **>(&tables), count * tw * sizeof(uint32_t), st) != cudaSuccess) {
+    cudaFreeAsync(d_ident, st);
+    if (d_rows) cudaFreeAsync(d_rows, st);
+    return cuda_fail("cudaMallocAsync(jump tables)");
   }
+  // pageable source: staged by the driver before the call returns
   int rc = cudaMemcpyAsync(d_ident, ident.data(), ident.size(), cudaMemcpyHostToDevice, st) == cudaSuccess
                ? SLP_OK
                : cuda_fail("cudaMemcpyAsync(identity)");
@@ -383,73 +474,54 @@ static int build_jump_tables(int id, const uint64_t *d_polys, uint64_t first_pol
     rc = ops->jump(p, host_poly ? &base : nullptr, true, 1, st);
     if (rc == SLP_OK) rc = ops->build_table(d_rows, tables + i * tw, st);
   }
-  if (rc == SLP_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail("jump tables");
-  cudaFree(d_ident);
-  cudaFree(d_rows);
+  cudaFreeAsync(d_ident, st);  // after the kernels above (stream order)
+  cudaFreeAsync(d_rows, st);
   if (rc != SLP_OK) {
-    cudaFree(tables);
+    cudaFreeAsync(tables, st);
     return rc;
   }
   *out = tables;
   return SLP_OK;
 }
 
+// K1t tables of an init plan's round polynomials
 static int plan_tables_on_device(const InitPlan &plan, int id, int dev, const uint64_t *d_polys, cudaStream_t st,
-                                 const DevTables **out) {
-  std::lock_guard<std::mutex> lk(g_dev_mu);
-  auto key = std::make_pair(&plan, dev);
-  auto it = g_dev_tables.find(key);
-  if (it != g_dev_tables.end()) {
-    *out = &it->second;
-    return SLP_OK;
-  }
-  DevTables t;
-  t.first_poly = plan.launches.size() > 1 ? plan.launches[1].poly0 : plan.polys.size() / plan.pw;
-  t.count = plan.polys.size() / plan.pw - t.first_poly;
-  // bounded: at most kMaxPlanTableSets table sets per device (a set is
-  // n^2/2 bytes per round polynomial: 0.7 MB for n = 256, 11 MB for
-  // n = 1024); further plans keep K1 for their rounds
-  static std::map<int, int> sets_per_dev;
-  constexpr int kMaxPlanTableSets = 64;
-  if (t.count > 0 && sets_per_dev[dev] < kMaxPlanTableSets) {
-    const int rc = build_jump_tables(id, d_polys, t.first_poly, nullptr, t.count, st, &t.tables);
+                                 Pinned &pin) {
+  const DevKey key{CACHE_PLAN_TABLES, dev, {plan.uid}};
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  pin.st = st;
+  if ((pin.e = cache_find(key, st))) return SLP_OK;
+  auto e = std::make_unique<DevEntry>();
+  e->first_poly = plan.launches.size() > 1 ? plan.launches[1].poly0 : plan.polys.size() / plan.pw;
+  e->count = plan.polys.size() / plan.pw - e->first_poly;
+  if (e->count > 0) {
+    uint32_t *t = nullptr;
+    const int rc = build_jump_tables(id, d_polys, e->first_poly, nullptr, e->count, st, &t);
     if (rc != SLP_OK) return rc;
-    ++sets_per_dev[dev];
-  } else {
-    t.count = 0;
+    e->ptr = t;
+    e->bytes = e->count * gen_ops(id)->table_words() * sizeof(uint32_t);
   }
-  auto res = g_dev_tables.emplace(key, t);
-  *out = &res.first->second;
+  pin.e = cache_insert(key, std::move(e), st);
   return SLP_OK;
 }
 
-// K1t tables of single jump polynomials (slp_jump_states), per (engine,
-// device, polynomial); at most kMaxPolyTables per device, never evicted
-// (a table may be in use on any stream), K1 once the cache is full
-constexpr size_t kMaxPolyTables = 32;
-static std::map<std::tuple<int, int, std::vector<uint64_t>>, uint32_t *> g_poly_tables;
-static std::map<int, size_t> g_poly_tables_per_dev;
-
-static int poly_table_on_device(int id, int dev, const uint64_t *poly, cudaStream_t st, const uint32_t **out) {
+// K1t table of a single jump polynomial (slp_jump_states), per (engine, device, polynomial)
+static int poly_table_on_device(int id, int dev, const uint64_t *poly, cudaStream_t st, Pinned &pin) {
   const GenDesc &g = *gen_desc(id);
-  std::vector<uint64_t> pv(poly, poly + g.n() / 64);
-  std::lock_guard<std::mutex> lk(g_dev_mu);
-  auto key = std::make_tuple(engine_id(id), dev, pv);
-  auto it = g_poly_tables.find(key);
-  if (it != g_poly_tables.end()) {
-    *out = it->second;
-    return SLP_OK;
-  }
-  if (g_poly_tables_per_dev[dev] >= kMaxPolyTables) {
-    *out = nullptr;
-    return SLP_OK;
-  }
+  std::vector<uint64_t> kw(poly, poly + g.n() / 64);
+  kw.push_back((uint64_t)engine_id(id));
+  const DevKey key{CACHE_POLY_TABLE, dev, kw};
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  pin.st = st;
+  if ((pin.e = cache_find(key, st))) return SLP_OK;
   uint32_t *t = nullptr;
-  const int rc = build_jump_tables(id, nullptr, 0, pv.data(), 1, st, &t);
+  const int rc = build_jump_tables(id, nullptr, 0, poly, 1, st, &t);
   if (rc != SLP_OK) return rc;
-  g_poly_tables[key] = t;
-  ++g_poly_tables_per_dev[dev];
-  *out = t;
+  auto e = std::make_unique<DevEntry>();
+  e->ptr = t;
+  e->bytes = gen_ops(id)->table_words() * sizeof(uint32_t);
+  e->count = 1;
+  pin.e = cache_insert(key, std::move(e), st);
   return SLP_OK;
 }
 
@@ -487,25 +559,27 @@ extern "C" {
 static int plan_rounds(const InitPlan &plan, int id, const GenOps *ops, int dev, const uint64_t *d_polys,
                        void *states, uint64_t ld, uint64_t n, uint64_t nblocks, cudaStream_t st) {
   int rc = SLP_OK;
-  const DevTables *tabs = nullptr;
+  Pinned tpin;  // the plan's K1t table set, pinned until the launches below are enqueued
+  const DevEntry *tabs = nullptr;
   for (size_t li = 1; li < plan.launches.size(); ++li) {
     InitLaunch L = plan.launches[li];
     if (L.dst0 >= n) break;
     if (L.count > n - L.dst0) L.count = n - L.dst0;
     if (L.uniform && use_jump_tables(L.count * nblocks)) {
       if (!tabs) {
-        rc = plan_tables_on_device(plan, id, dev, d_polys, st, &tabs);
+        rc = plan_tables_on_device(plan, id, dev, d_polys, st, tpin);
         if (rc != SLP_OK) return rc;
+        tabs = tpin.e;
       }
     }
-    if (L.uniform && tabs && tabs->tables && use_jump_tables(L.count * nblocks)) {
+    if (L.uniform && tabs && tabs->ptr && use_jump_tables(L.count * nblocks)) {
       TableJumpParams tp{};
       tp.rt = gen_rt(id);
       tp.src = states;
       tp.ld_src = ld;
       tp.dst = states;
       tp.ld_dst = ld;
-      tp.tables = tabs->tables;
+      tp.tables = static_cast<const uint32_t *>(tabs->ptr);
       tp.table0 = L.poly0 - tabs->first_poly;
       tp.count = L.count;
       tp.m = L.m;
@@ -548,9 +622,9 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
     return SLP_ERR_INVALID;
   for (uint64_t b = 0; b < nblocks; ++b)
     if (!state_ok(*g, base_flat + b * g->k)) return SLP_ERR_ZERO_STATE;
-  const InitPlan *plan;
+  std::shared_ptr<const InitPlan> plan;
   try {
-    plan = &init_plan(id, steps, steps_words, n);
+    plan = init_plan(id, steps, steps_words, n);
   } catch (const AlgebraError &e) {
     set_last_error(e.what());
     return SLP_ERR_ALGEBRA;
@@ -560,10 +634,11 @@ int slp_init_substreams(int id, const uint64_t *base_flat, uint64_t nblocks, con
   }
   const int dev = current_device();
   if (dev < 0) return cuda_fail("cudaGetDevice");
-  const uint64_t *d_polys = nullptr;
-  int rc = plan_polys_on_device(*plan, dev, &d_polys);
-  if (rc != SLP_OK) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Pinned ppin;  // the plan's device polynomials, pinned until every launch is enqueued
+  int rc = plan_polys_on_device(*plan, dev, st, ppin);
+  if (rc != SLP_OK) return rc;
+  const uint64_t *d_polys = static_cast<const uint64_t *>(ppin.e->ptr);
   const size_t esize = g->w / 8;
   // launch 0: every block base -> first m0 substreams (one polynomial per substream)
   const InitLaunch &l0 = plan->launches[0];
@@ -602,9 +677,9 @@ int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, co
   if (!states || !seg_states || ld < n || ld_seg < n * J || seg_words < 0 || (seg_words > 0 && !seg_steps) ||
       J > (1ull << 20))
     return SLP_ERR_INVALID;
-  const InitPlan *plan;
+  std::shared_ptr<const InitPlan> plan;
   try {
-    plan = &init_plan(id, seg_steps, seg_words, J);  // segment j = substream jumped by x^(j*seg)
+    plan = init_plan(id, seg_steps, seg_words, J);  // segment j = substream jumped by x^(j*seg)
   } catch (const AlgebraError &e) {
     set_last_error(e.what());
     return SLP_ERR_ALGEBRA;
@@ -614,10 +689,11 @@ int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, co
   }
   const int dev = current_device();
   if (dev < 0) return cuda_fail("cudaGetDevice");
-  const uint64_t *d_polys = nullptr;
-  int rc = plan_polys_on_device(*plan, dev, &d_polys);
-  if (rc != SLP_OK) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Pinned ppin;  // the plan's device polynomials, pinned until every launch is enqueued
+  int rc = plan_polys_on_device(*plan, dev, st, ppin);
+  if (rc != SLP_OK) return rc;
+  const uint64_t *d_polys = static_cast<const uint64_t *>(ppin.e->ptr);
   const size_t esize = g->w / 8;
   // the init plan with the n substreams as its batches: launch 0 jumps each
   // substream directly into its first segments, the radix rounds grow the rest
@@ -696,10 +772,11 @@ int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *sr
   if (count >= kJumpTableMinStates && (src != dst || g->n() <= 256) && use_jump_tables(count)) {
     const int dev = current_device();
     if (dev < 0) return cuda_fail("cudaGetDevice");
-    const uint32_t *table = nullptr;
-    const int rc = poly_table_on_device(id, dev, base.w, st, &table);
+    Pinned tpin;
+    const int rc = poly_table_on_device(id, dev, base.w, st, tpin);
     if (rc != SLP_OK) return rc;
-    if (table) {
+    const uint32_t *table = static_cast<const uint32_t *>(tpin.e->ptr);
+    {
       TableJumpParams tp{};
       tp.rt = gen_rt(id);
       tp.src = src;
@@ -998,6 +1075,12 @@ int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, ui
   p.overflow_ctas = reinterpret_cast<unsigned long long *>(overflow_ctas);
   if (nthreads == 0) return SLP_OK;
   return ops->hwd(p, transitional, split, static_cast<cudaStream_t>(stream));
+}
+
+size_t slp_device_cache_bytes(int device) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_cache_bytes.find(device);
+  return it == g_cache_bytes.end() ? 0 : it->second;
 }
 
 const char *slp_build_info(void) {

@@ -558,10 +558,21 @@ struct PlanKey {
   bool operator<(const PlanKey &o) const { return std::tie(eid, steps, n) < std::tie(o.eid, o.steps, o.n); }
 };
 
+// bounded LRU: plans are keyed by the exact stride (segment split: T / J,
+// lane_len, HWD segment lengths), so a long-running caller may see many;
+// callers hold a shared_ptr for the duration of a call, so eviction never
+// pulls a plan from under a launch.  Device copies are keyed by InitPlan::uid
+// (slp_api.cu) and age out of their own LRU.
+static constexpr size_t kMaxPlans = 256;
 static std::mutex g_plan_mu;
-static std::map<PlanKey, std::unique_ptr<InitPlan>> g_plans;
+struct PlanSlot {
+  std::shared_ptr<const InitPlan> plan;
+  uint64_t tick;
+};
+static std::map<PlanKey, PlanSlot> g_plans;
+static uint64_t g_plan_tick = 0, g_plan_uid = 0;
 
-const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64_t n_req) {
+std::shared_ptr<const InitPlan> init_plan(int id, const uint64_t *steps, int steps_words, uint64_t n_req) {
   const int eid = engine_id(id);
   std::vector<uint64_t> st(steps, steps + steps_words);
   while (!st.empty() && st.back() == 0) st.pop_back();
@@ -577,11 +588,14 @@ const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_plans.find(key);
-    if (it != g_plans.end()) return *it->second;
+    if (it != g_plans.end()) {
+      it->second.tick = ++g_plan_tick;
+      return it->second.plan;
+    }
   }
   const GenDesc &g = *gen_desc(eid);
   const Poly &P = engine_char_poly(eid);
-  auto plan = std::make_unique<InitPlan>();
+  auto plan = std::make_shared<InitPlan>();
   const int pw = (g.n() + 63) / 64;
   plan->pw = pw;
   auto push = [&](const Poly &p) {
@@ -623,8 +637,21 @@ const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64
     xmJ = pc;
   }
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  auto res = g_plans.emplace(std::move(key), std::move(plan));
-  return *res.first->second;
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) {  // built concurrently by another thread
+    it->second.tick = ++g_plan_tick;
+    return it->second.plan;
+  }
+  while (g_plans.size() >= kMaxPlans) {
+    auto lru = g_plans.begin();
+    for (auto jt = g_plans.begin(); jt != g_plans.end(); ++jt)
+      if (jt->second.tick < lru->second.tick) lru = jt;
+    g_plans.erase(lru);
+  }
+  plan->uid = ++g_plan_uid;
+  std::shared_ptr<const InitPlan> cp = plan;
+  g_plans.emplace(std::move(key), PlanSlot{cp, ++g_plan_tick});
+  return cp;
 }
 
 }  // namespace slp
@@ -776,7 +803,8 @@ int slp_register_generator(const slp_gen_info *spec) {
   c->d = g;
   c->d.id = SLP_CUSTOM_ID0 + n;
   std::memset(c->name, 0, sizeof c->name);
-  std::strncpy(c->name, spec->name[0] ? spec->name : "custom", sizeof(c->name) - 1);
+  const char *nm = spec->name[0] ? spec->name : "custom";
+  std::memcpy(c->name, nm, strnlen(nm, sizeof(c->name) - 1));  // spec->name need not be terminated
   c->d.name = c->name;
   g_custom[n] = std::move(c);
   g_ncustom.store(n + 1, std::memory_order_release);

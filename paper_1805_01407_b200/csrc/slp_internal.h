@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -69,11 +70,10 @@ struct InitPlan {
   int pw;  // words per poly = ceil(n / 64)
   std::vector<uint64_t> polys;  // npolys * pw
   std::vector<InitLaunch> launches;
-  // device copy (owned by the plan cache)
-  void *d_polys = nullptr;
-  int device = -1;
+  uint64_t uid = 0;  // unique per built plan: key of its device copies (slp_api.cu)
 };
-const InitPlan &init_plan(int id, const uint64_t *steps, int steps_words, uint64_t n);
+// cached (bounded LRU); hold the pointer for the duration of a call
+std::shared_ptr<const InitPlan> init_plan(int id, const uint64_t *steps, int steps_words, uint64_t n);
 
 void set_last_error(const std::string &s);
 

@@ -7,7 +7,7 @@ import pytest
 
 from oracle import oracle as O
 
-NAMES = list(O.SPECS)
+NAMES = O.REGISTRY_NAMES
 
 
 def hexs(vals):
