@@ -275,14 +275,15 @@ def fill_to_host(spec: GeneratorSpec, states: torch.Tensor, T: int, host_out: to
         raise ValueError(f"host_out dtype must be {dt}")
     sl = max(1, min(slice_streams, n))
     bufs = _bufs if _bufs is not None else [torch.empty((sl, T), dtype=dt, device=dev) for _ in range(2)]
+    nb = len(bufs)
     compute = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
-    done = [None, None]
+    done = [None] * nb
     for i, a in enumerate(range(0, n, sl)):
         b = min(n, a + sl)
-        buf = bufs[i & 1][: b - a]
-        if done[i & 1] is not None:
-            compute.wait_event(done[i & 1])
+        buf = bufs[i % nb][: b - a]
+        if done[i % nb] is not None:
+            compute.wait_event(done[i % nb])
         fill(spec, states[:, a:b], T, out=buf, kind=kind)
         ready = torch.cuda.Event()
         ready.record(compute)
@@ -291,7 +292,7 @@ def fill_to_host(spec: GeneratorSpec, states: torch.Tensor, T: int, host_out: to
             host_out[a:b].copy_(buf, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(copy)
-        done[i & 1] = ev
+        done[i % nb] = ev
     compute.wait_stream(copy)
     return host_out
 
