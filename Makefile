@@ -1,5 +1,5 @@
 # Builds the in-tree C-ABI library paper_1805_01407_b200/_lib/libslp_b200.so
-# (sm_100a only) and the CPU oracle oracle/_build/liboracle.so (test-only).
+# (sm_100a only).  The CPU oracle (oracle/) is numpy and needs no build.
 NVCC ?= /usr/local/cuda/bin/nvcc
 CSRC := paper_1805_01407_b200/csrc
 LIBDIR := paper_1805_01407_b200/_lib
@@ -12,7 +12,7 @@ INST := $(wildcard $(CSRC)/slp_inst_*.cu)
 OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(INST)) $(OBJDIR)/slp_api.o $(OBJDIR)/slp_host.o
 HDRS := $(wildcard $(CSRC)/*.h $(CSRC)/*.cuh) include/slp_b200.h
 
-all: $(LIBDIR)/libslp_b200.so oracle
+all: $(LIBDIR)/libslp_b200.so
 
 # A/B experiment builds: make variant VARIANT=name EXTRA="-DSLP_ROT_POLICY=0"
 variant: variants/libslp_$(VARIANT).so
@@ -33,11 +33,7 @@ $(LIBDIR)/libslp_b200.so: $(OBJS)
 	@mkdir -p $(LIBDIR)
 	$(NVCC) -shared $(ARCH) -cudart static -o $@ $(OBJS)
 
-oracle:
-	$(MAKE) -C oracle
-
 clean:
 	rm -rf build $(LIBDIR)/*.so
-	$(MAKE) -C oracle clean
 
-.PHONY: all clean oracle variant
+.PHONY: all clean variant

@@ -22,6 +22,7 @@ from __future__ import annotations
 import ctypes
 import math
 import os
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -124,6 +125,18 @@ class HwdConfig:
             self.C = self.k // 2 + 1
         if not 1 <= self.C <= self.k:
             raise ValueError("C must be in 1..k")
+        if self.batch_size is not None:
+            if self.batch_size < 1:
+                raise ValueError("batch_size must be positive")
+            # the reference (hwd.py:167-247, 543-555) flushes 13/19-bit packed
+            # counters every batch_size values and reports a forced failure
+            # (p = 1e-100, overflow=True) when one overflowed; its default
+            # sizing makes that a <= 1e-100 event.  The GPU counters are exact,
+            # so a caller-chosen batch size that would overflow there does not
+            # fail here.
+            warnings.warn("HwdConfig.batch_size is ignored: the GPU counters are exact; the reference's "
+                          "per-batch overflow failure (hwd.py:543-555) is not reproduced", RuntimeWarning,
+                          stacklevel=3)
 
 
 @dataclass

@@ -108,9 +108,14 @@ def test_hwd_stdin_rejected(capsys):
 
 
 @pytest.mark.gpu
-def test_hwd_cli_detects_xorshift128plus(capsys):
+def test_hwd_cli_detects_xorshift128plus(capsys, G):
+    """The paper row through the CLI (reference cli.py:122-160): the JSON report
+    equals the reference's own report for the same run (tests/golden/hwd.json)."""
+    key = "xorshift128plus/1/None/batch_size=2300000,byte_limit=24000000000,k=8,mode=transitional,w=64"
+    want = {k: v for k, v in G("hwd")[key].items()
+            if k not in ("name", "seed", "checkpoint_start", "config", "ref_seconds")}
     code, out, _ = run_cli(capsys, "hwd", "--algo", "xorshift128plus", "--mode", "transitional",
-                           "--limit", "2.4e10", "--json")
+                           "--limit", "2.4e10", "--seed", "1", "--json")
     assert code == 3
-    doc = json.loads(out)
-    assert doc["status"] == "failed" and doc["signature"] in ("00000012", "00000021")
+    assert json.loads(out) == want
+    assert want["status"] == "failed" and want["signature"] == "00000021"

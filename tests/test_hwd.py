@@ -73,7 +73,11 @@ def test_run_generator_matches_reference(G, idx):
     if idx >= len(cases):
         pytest.skip("golden case not generated")
     key, d = cases[idx]
-    cfg = hwd.HwdConfig(**d["config"])
+    if d["config"].get("batch_size") is not None:
+        with pytest.warns(RuntimeWarning, match="batch_size is ignored"):
+            cfg = hwd.HwdConfig(**d["config"])
+    else:
+        cfg = hwd.HwdConfig(**d["config"])
     rep = hwd.run_generator(d["name"], cfg, seed=d["seed"], checkpoint_start=d["checkpoint_start"]).to_dict()
     want = {k: v for k, v in d.items() if k not in ("name", "seed", "checkpoint_start", "config", "ref_seconds")}
     assert rep == want, key
@@ -82,7 +86,8 @@ def test_run_generator_matches_reference(G, idx):
 @pytest.mark.gpu
 def test_paper_row_xorshift128plus_transitional_detected():
     """test_hwd.py:286-296 of the reference (marked slow there: hours in numpy)."""
-    cfg = hwd.HwdConfig(w=64, k=8, byte_limit=int(2.4e10), batch_size=2_300_000, mode="transitional")
+    with pytest.warns(RuntimeWarning):
+        cfg = hwd.HwdConfig(w=64, k=8, byte_limit=int(2.4e10), batch_size=2_300_000, mode="transitional")
     rep = hwd.run_generator("xorshift128plus", cfg, seed=1, lanes=16384, lane_len=1024)
     assert rep.status == "failed"
     assert rep.bytes_processed <= 2.4e10
@@ -92,7 +97,8 @@ def test_paper_row_xorshift128plus_transitional_detected():
 @pytest.mark.gpu
 def test_paper_row_xoshiro256starstar_passes():
     """test_hwd.py:298-304 of the reference."""
-    cfg = hwd.HwdConfig(w=64, k=8, byte_limit=int(1e10), batch_size=2_300_000)
+    with pytest.warns(RuntimeWarning):
+        cfg = hwd.HwdConfig(w=64, k=8, byte_limit=int(1e10), batch_size=2_300_000)
     rep = hwd.run_generator("xoshiro256starstar", cfg, seed=1, lanes=16384, lane_len=1024)
     assert rep.status == "passed"
     assert rep.p_value > 1e-20
