@@ -5,10 +5,20 @@ CSRC := paper_1805_01407_b200/csrc
 LIBDIR := paper_1805_01407_b200/_lib
 OBJDIR := build/obj$(if $(VARIANT),_$(VARIANT),)
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall -Xptxas -v -I include $(EXTRA)
+NVFLAGS = -O3 -std=c++17 $(ARCH) $(NVFLAGS_LINE) -Xcompiler -fPIC -Xcompiler -Wall -Xptxas -v -I include $(EXTRA)
 CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -I include
 
+# A/B variant builds (VARIANT=name) leave out the run-time parameter
+# (custom-engine) instances and -lineinfo: they only time registry kernels,
+# and must stay small enough to ship to the GPU box next to the main library
 INST := $(wildcard $(CSRC)/slp_inst_*.cu)
+ifneq ($(VARIANT),)
+INST := $(filter-out $(CSRC)/slp_inst_rt%.cu,$(INST))
+override EXTRA += -DSLP_NO_RT_INSTANCES
+NVFLAGS_LINE :=
+else
+NVFLAGS_LINE := -lineinfo
+endif
 OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(INST)) $(OBJDIR)/slp_api.o $(OBJDIR)/slp_host.o
 HDRS := $(wildcard $(CSRC)/*.h $(CSRC)/*.cuh) include/slp_b200.h
 

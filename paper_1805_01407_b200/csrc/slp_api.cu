@@ -24,10 +24,15 @@ SLP_PART_DECL(2)
 SLP_PART_DECL(3)
 SLP_PART_DECL(4)
 SLP_PART_DECL(5)
+#ifdef SLP_NO_RT_INSTANCES  // A/B variant builds (Makefile): registry kernels only
+static const ::slp::GenOps slp_ops_rt_0[SLP_NUM_RT_SHAPES] = {}, slp_ops_rt_1[SLP_NUM_RT_SHAPES] = {},
+                           slp_ops_rt_2[SLP_NUM_RT_SHAPES] = {};
+#else
 #define SLP_RT_PART_DECL(P) extern const ::slp::GenOps slp_ops_rt_##P[SLP_NUM_RT_SHAPES];
 SLP_RT_PART_DECL(0)
 SLP_RT_PART_DECL(1)
 SLP_RT_PART_DECL(2)
+#endif
 
 namespace slp {
 
@@ -61,6 +66,7 @@ const GenOps *gen_ops(int id) {
 // run-time parameters of a generator for the GenR<> instances
 GenRt gen_rt(int id) {
   GenRt r{};
+  r.one = r.one2 = 1;
   const GenDesc *g = gen_desc(id);
   if (!g) return r;
   r.a = (uint32_t)g->a;

@@ -41,7 +41,11 @@ __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedPa
   // is an opaque 1 from the parameters so ptxas cannot turn it into IADD3);
   // together they give the EXACT sum.  xor: one 3-input LOP3 per output pair
   // and half.  MANT: low-bit sum = LOP3 + IMAD.
+#ifdef SLP_FUSED_MASK  // A/B: force the FMA-form rotation sites (masked to the generator's sites)
+  constexpr int MSK = SLP_FUSED_MASK & G::kSites;
+#else
   constexpr int MSK = G::best_mask(G::w == 64 ? 1 : 1, (G::w == 64 ? 2 : 1) + (MANT ? 1 : 0));
+#endif
   const uint32_t one = p.one;
   uint64_t slo = 0, shi = 0, sx = 0, slow = 0;
   double fs = 0.0, fs2 = 0.0;

@@ -64,6 +64,9 @@ __device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {
 //            Gen::best_mask with SLP_ROT_POLICY=1 loses to IMAD.WIDE's rate)
 //   shl    : IMAD.SHL (low half) + SHF.L.U64.HI          -> 1 FMA + 1 ALU
 //   mulc   : IMAD.WIDE + IMAD (+ IMAD for a 64-bit constant).
+#ifndef SLP_ROTH_FORM
+#define SLP_ROTH_FORM 1  // rotl_h low halves: 1 constant shifts, 0 mul.lo by an opaque 2^r
+#endif
 #ifndef SLP_MUL_POLICY
 #define SLP_MUL_POLICY 1  // 0: shifts via IMAD.WIDE; 1: 64-bit constant shifts as IMAD.SHL + SHF; 2: also x*(2^a+1) as LEA pairs
 #endif
@@ -81,6 +84,10 @@ struct WOps<32> {
   template <int R>
   static __device__ __forceinline__ word rotl_f(word x) {
     return __funnelshift_l(x, x, R);  // no cheaper FMA form for one 32-bit word
+  }
+  template <int R>
+  static __device__ __forceinline__ word rotl_h(word x, uint32_t, uint32_t) {
+    return __funnelshift_l(x, x, R);
   }
   template <int B>
   static __device__ __forceinline__ word shl(word x) {
@@ -130,6 +137,36 @@ struct WOps<64> {
     const uint64_t w3 = madw(l, m, w2 >> 32);                // low: (l << r) | (h >> (32 - r))
     return pack((uint32_t)w3, (uint32_t)w2);
   }
+  // rotation with its cross-word halves on the FMA pipe: with m = 2^(R mod 32)
+  // in a register ptxas cannot see through (Gen::one2), lo' = hi(h*m) +
+  // (l << r) and hi' = hi(l*m) + (h << r) (disjoint bits): two IMAD.HI (half
+  // the ALU rate, profiles/int_peak.cu) plus two constant shifts (SHF or
+  // IMAD.SHL, ptxas's choice) instead of two SHF.L.W on the saturated ALU
+  // pipe.  (Low products as mul.lo by an opaque m2, SLP_ROTH_FORM=0, made
+  // ptxas fuse lo(l*m) with hi(l*m) into a quarter-rate IMAD.WIDE.)
+  template <int R>
+  static __device__ __forceinline__ word rotl_h(word x, uint32_t m, uint32_t m2) {
+    uint32_t l = lo(x), h = hi(x);
+    if constexpr (R >= 32) {
+      const uint32_t t = l;
+      l = h;
+      h = t;
+    }
+    if constexpr ((R & 31) == 0) return pack(l, h);
+    constexpr int r = R & 31;
+#if SLP_ROTH_FORM == 1
+    const uint32_t ll = l << r, hl = h << r;
+    (void)m2;
+#else
+    uint32_t ll, hl;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(ll) : "r"(l), "r"(m2));
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(hl) : "r"(h), "r"(m2));
+#endif
+    uint32_t nl, nh;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(nl) : "r"(h), "r"(m), "r"(ll));
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(nh) : "r"(l), "r"(m), "r"(hl));
+    return pack(nl, nh);
+  }
   template <int B>
   static __device__ __forceinline__ word shl(word x) {
 #if SLP_MUL_POLICY >= 1
@@ -165,7 +202,9 @@ struct WOps<64> {
 // Build-time policy switches (A/B experiments, profiles/): rotation pipe
 // balancing and the fused accumulator form.
 #ifndef SLP_ROT_POLICY
-#define SLP_ROT_POLICY 0  // 0: all rotations on the ALU; 1: Gen::best_mask (A/B: no gain, ptxas re-normalises)
+// 0: all rotations on the ALU; 1: Gen::best_mask with 3-IMAD.WIDE rotations
+// (A/B: slower); 2: Gen::best_mask with IMAD + IMAD.HI rotations (rotl_h)
+#define SLP_ROT_POLICY 0
 #endif
 #ifndef SLP_SUM_POLICY
 #define SLP_SUM_POLICY 3  // 0: 128-bit carry chain per output; 1, 2: IMAD.WIDE accumulators; 3: half sums
@@ -192,8 +231,14 @@ struct Gen {
   static constexpr bool runtime = false;
   // kernels call the generator through an object (`eng.step(...)`) so that
   // the same code serves GenR<> below, whose parameters are run-time values;
-  // for Gen<> the object is empty and every member is static
-  static __device__ __forceinline__ Gen load(const GenRt &) { return Gen{}; }
+  // Gen<> only carries the opaque 1 that the FMA-pipe rotations multiply by
+  uint32_t one, one2;
+  static __device__ __forceinline__ Gen load(const GenRt &rt) {
+    Gen g;
+    g.one = rt.one;
+    g.one2 = rt.one2;
+    return g;
+  }
 
   // Rotation sites that may run on either pipe (bit set in a mask = FMA form):
   //   bit 0: engine rotation by A (xoroshiro) / by B (xoshiro)
@@ -232,15 +277,19 @@ struct Gen {
     for (int m = 0; m < 8; ++m) {
       if ((m & ~kSites) != 0) continue;
       int alu = f.alu + extra_alu, fma = f.fma + extra_fma;
+      int fma_hi = 0;  // IMAD.HI: half rate on the FMA pipe
       for (int bit = 0; bit < 3; ++bit) {
         if (!(kSites & (1 << bit))) continue;
-        if (m & (1 << bit))
-          fma += 3;
-        else
+        if (!(m & (1 << bit)))
           alu += 2;
+        else if (SLP_ROT_POLICY == 2)
+          fma += 2, fma_hi += 2;  // rotl_h: 2 IMAD + 2 IMAD.HI
+        else
+          fma += 3;  // rotl_f: 3 IMAD.WIDE (counted as IMAD; measured slower)
       }
-      const int cost = (2 * alu > 2 * fma ? 2 * alu : 2 * fma) > alu + fma ? (2 * alu > 2 * fma ? 2 * alu : 2 * fma)
-                                                                            : alu + fma;
+      // cycles x 2 per SM: ALU and FMA pipes at 2 warp-inst/clk, dispatch at 4
+      const int c_alu = 2 * alu, c_fma = 2 * (fma + 2 * fma_hi), c_disp = alu + fma + fma_hi;
+      const int cost = c_alu > c_fma ? (c_alu > c_disp ? c_alu : c_disp) : (c_fma > c_disp ? c_fma : c_disp);
       if (cost < best_cost) {
         best_cost = cost;
         best = m;
@@ -250,8 +299,10 @@ struct Gen {
   }
 
   template <int M, int RR>
-  static __device__ __forceinline__ word rot(word x) {
-    if constexpr (M != 0)
+  __device__ __forceinline__ word rot(word x) const {
+    if constexpr (M != 0 && SLP_ROT_POLICY == 2)
+      return O::template rotl_h<RR>(x, one << (RR & 31), one2 << (RR & 31));
+    else if constexpr (M != 0)
       return O::template rotl_f<RR>(x);
     else
       return O::template rotl<RR>(x);
@@ -262,7 +313,7 @@ struct Gen {
 
   // scramblers.py:84-95, applied to the current (pre-step) state
   template <int M>
-  static __device__ __forceinline__ word output_m(const word (&s)[K], int o) {
+  __device__ __forceinline__ word output_m(const word (&s)[K], int o) const {
     const word xi = s[slot(o, WI)];
     if constexpr (SC == SLP_SC_NONE) {
       return xi;
@@ -280,7 +331,7 @@ struct Gen {
   // one engine step in the flat view (engines.py:100-140).  For ring engines
   // the flat view moves by one slot: the caller's next offset is o + 1.
   template <int M>
-  static __device__ __forceinline__ void step_m(word (&s)[K], int o) {
+  __device__ __forceinline__ void step_m(word (&s)[K], int o) const {
     if constexpr (FAM == SLP_FAM_XOROSHIRO) {
       const int i0 = slot(o, 0), il = slot(o, K - 1);
       const word x0 = s[i0];
@@ -316,11 +367,11 @@ struct Gen {
   }
 
   // defaults (all-ALU rotations): jump kernel and tails
-  static __device__ __forceinline__ word output(const word (&s)[K], int o) { return output_m<0>(s, o); }
-  static __device__ __forceinline__ void step(word (&s)[K], int o) { step_m<0>(s, o); }
+  __device__ __forceinline__ word output(const word (&s)[K], int o) const { return output_m<0>(s, o); }
+  __device__ __forceinline__ void step(word (&s)[K], int o) const { step_m<0>(s, o); }
 
   // one output + step, registers left in flat order (tails of odd length)
-  static __device__ __forceinline__ word next_flat(word (&s)[K]) {
+  __device__ __forceinline__ word next_flat(word (&s)[K]) const {
     const word out = output(s, 0);
     step(s, 0);
     if constexpr (ring) {

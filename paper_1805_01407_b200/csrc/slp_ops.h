@@ -16,6 +16,7 @@ struct GenRt {
   int32_t sc, wi, wj;   // scrambler kind (SLP_SC_*) and flat word indices (wj < 0: unused)
   uint32_t R;           // scrambler rotation (++ and **)
   uint64_t S, T;        // scrambler multipliers (* and **)
+  uint32_t one, one2;   // = 1, opaque to ptxas: multipliers 2^r for FMA-pipe rotations (Gen::rot)
 };
 
 struct FillParams {
