@@ -144,8 +144,10 @@ int slp_jump_states(int id, const uint64_t *poly, int poly_words, const void *sr
 int slp_split_substreams(int id, const void *states, uint64_t ld, uint64_t n, const uint64_t *seg_steps,
                          int seg_words, uint64_t J, void *seg_states, uint64_t ld_seg, void *stream);
 
-/* Segments per substream that slp_fill (stream-major, ld_out == T),
- * slp_fill_checksum and slp_fused use internally for n substreams of T
+/* Segments per substream that slp_fill (stream-major contiguous rows;
+ * padded stream-major rows when the output, its 16-byte row pitch and the
+ * segment length are TMA-addressable; position-major), slp_fill_checksum
+ * (contiguous rows) and slp_fused use internally for n substreams of T
  * outputs: 1 from 2^15 substreams up (one thread per substream fills the
  * GPU); else a power of two J dividing T, doubled up to n*J = 2^14 while
  * segments keep >= max(512, 2 * state bits) outputs, then up to 2^18 while

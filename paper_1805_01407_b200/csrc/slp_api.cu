@@ -147,22 +147,28 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// Stream-major output [nstreams][ld_out] viewed as a 3-D tensor
-// (element within a 128-byte segment, substream, segment index) so that one
-// box {128/es, 32, segs} is 32 substreams x segs contiguous segments.
+// Stream-major output viewed as a 4-D tensor (element within a 128-byte
+// piece, segment j, substream i, piece index): rows are the `nstreams`
+// segments v = i * J + j (J = 1 << jsh, T outputs each) of nstreams >> jsh
+// substreams with row pitch ld_out, segment j at column j * T -- J = 1 is the
+// plain [nstreams][ld_out] layout.  One box {128/es, Jb, 32/Jb, segs},
+// Jb = min(J, 32), is the 32 segment rows of a warp x segs contiguous
+// pieces; in shared memory its lines come out in warp-row order
+// ((seg * 32 + lane) * 128 B), the layout of k_fill's tile.
 int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out,
-                    int segs) {
+                    int segs, int jsh) {
   auto fn = encode_fn();
   if (!fn) {
     set_last_error("cuTensorMapEncodeTiled unavailable");
     return SLP_ERR_CUDA;
   }
   const uint64_t seg = 128 / es;
-  cuuint64_t gdim[3] = {(cuuint64_t)seg, (cuuint64_t)nstreams, (cuuint64_t)(T / seg)};
-  cuuint64_t gstride[2] = {(cuuint64_t)(ld_out * es), 128};
-  cuuint32_t box[3] = {(cuuint32_t)seg, 32, (cuuint32_t)segs};
-  cuuint32_t estride[3] = {1, 1, 1};
-  CUresult r = fn(map, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, out, gdim,
+  const uint64_t J = 1ull << jsh, Jb = J < 32 ? J : 32;
+  cuuint64_t gdim[4] = {(cuuint64_t)seg, (cuuint64_t)J, (cuuint64_t)(nstreams >> jsh), (cuuint64_t)(T / seg)};
+  cuuint64_t gstride[3] = {(cuuint64_t)((J > 1 ? T : ld_out) * es), (cuuint64_t)(ld_out * es), 128};
+  cuuint32_t box[4] = {(cuuint32_t)seg, (cuuint32_t)Jb, (cuuint32_t)(32 / Jb), (cuuint32_t)segs};
+  cuuint32_t estride[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, out, gdim,
                   gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -302,11 +308,22 @@ __global__ void k_fused_final(const slp_checksum *parts, int nparts, slp_checksu
 }
 // states_out[j][i] = seg[j][i*J + J-1]: substream i ends where its last segment ends
 template <class W>
-__global__ void k_segment_ends(const W *seg, uint64_t n, uint64_t J, int k, W *out, uint64_t ld) {
+__global__ void k_segment_ends(const W *seg, uint64_t n, uint64_t J, int k, W *out, uint64_t ld, int jmajor) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * (uint64_t)k) return;
   const uint64_t j = t / n, i = t - j * n;
-  out[j * ld + i] = seg[j * n * J + i * J + J - 1];
+  out[j * ld + i] = seg[j * n * J + (jmajor ? (J - 1) * n + i : i * J + J - 1)];
+}
+// segment states i * J + j  ->  j * n + i (position-major split: a warp's
+// lanes are consecutive substreams of one row block), every word row
+template <class W>
+__global__ void k_segments_jmajor(const W *in, W *out, uint64_t n, uint64_t J, int k) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t m = n * J;
+  if (t >= m * (uint64_t)k) return;
+  const uint64_t w = t / m, v = t - w * m;  // v = j * n + i (coalesced writes)
+  const uint64_t j = v / n, i = v - j * n;
+  out[w * m + v] = in[w * m + i * J + j];
 }
 }  // namespace dev
 
@@ -852,7 +869,7 @@ struct Segments {
 }  // namespace
 
 static int make_segments(int id, const GenDesc &g, const void *states, uint64_t ld, uint64_t n, uint64_t T,
-                         uint64_t J, cudaStream_t st, Segments &seg) {
+                         uint64_t J, cudaStream_t st, Segments &seg, bool jmajor = false) {
   seg.st = st;
   const int dev = current_device();
   static std::atomic<int> pool_set[64];
@@ -866,24 +883,40 @@ static int make_segments(int id, const GenDesc &g, const void *states, uint64_t 
     }
     pool_set[dev] = 1;
   }
-  if (cudaMallocAsync(&seg.states, (size_t)g.k * n * J * (g.w / 8), st) != cudaSuccess) {
+  const size_t bytes = (size_t)g.k * n * J * (g.w / 8);
+  if (cudaMallocAsync(&seg.states, bytes, st) != cudaSuccess) {
     seg.states = nullptr;
     return cuda_fail("cudaMallocAsync(segments)");
   }
   const uint64_t steps[1] = {T / J};
-  return slp_split_substreams(id, states, ld, n, steps, 1, J, seg.states, n * J, st);
+  int rc = slp_split_substreams(id, states, ld, n, steps, 1, J, seg.states, n * J, st);
+  if (rc != SLP_OK || !jmajor) return rc;
+  void *tmp = nullptr;
+  if (cudaMallocAsync(&tmp, bytes, st) != cudaSuccess) return cuda_fail("cudaMallocAsync(segments)");
+  const uint64_t total = n * J * (uint64_t)g.k;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  if (g.w == 64)
+    slp::dev::k_segments_jmajor<uint64_t><<<blocks, 256, 0, st>>>(static_cast<const uint64_t *>(seg.states),
+                                                                  static_cast<uint64_t *>(tmp), n, J, g.k);
+  else
+    slp::dev::k_segments_jmajor<uint32_t><<<blocks, 256, 0, st>>>(static_cast<const uint32_t *>(seg.states),
+                                                                  static_cast<uint32_t *>(tmp), n, J, g.k);
+  rc = check_launch("k_segments_jmajor");
+  cudaFreeAsync(seg.states, st);
+  seg.states = tmp;
+  return rc;
 }
 
 static int segment_ends(const GenDesc &g, const Segments &seg, uint64_t n, uint64_t J, void *states_out, uint64_t ld,
-                        cudaStream_t st) {
+                        cudaStream_t st, int jmajor = 0) {
   const uint64_t total = n * (uint64_t)g.k;
   const unsigned blocks = (unsigned)((total + 255) / 256);
   if (g.w == 64)
     slp::dev::k_segment_ends<uint64_t><<<blocks, 256, 0, st>>>(static_cast<const uint64_t *>(seg.states), n, J, g.k,
-                                                          static_cast<uint64_t *>(states_out), ld);
+                                                          static_cast<uint64_t *>(states_out), ld, jmajor);
   else
     slp::dev::k_segment_ends<uint32_t><<<blocks, 256, 0, st>>>(static_cast<const uint32_t *>(seg.states), n, J, g.k,
-                                                          static_cast<uint32_t *>(states_out), ld);
+                                                          static_cast<uint32_t *>(states_out), ld, jmajor);
   return check_launch("k_segment_ends");
 }
 
@@ -920,18 +953,39 @@ int slp_fill(int id, const void *states_in, void *states_out, uint64_t ld, uint6
     return SLP_OK;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const uint64_t J = layout == SLP_STREAM_MAJOR && ld_out == T ? split_factor(*g, nstreams, T) : 1;
+  // few, long substreams: segment split.  Contiguous stream-major rows: the
+  // segments are plain rows of pitch T/J.  Padded stream-major rows: segment
+  // (i, j) is row i, column j*T/J, through the 4-D store map (TMA-addressable
+  // output only: 128-byte aligned base, 16-byte row pitch and segment
+  // length).  Position-major: segments in j-major order (lanes = consecutive
+  // substreams of one row block), written through the 2-D store map when a
+  // warp's segments share a row block, else with element stores.
+  uint64_t J = split_factor(*g, nstreams, T);
+  if (J > 1 && layout == SLP_STREAM_MAJOR && ld_out != T) {
+    const uint64_t es = out_kind == SLP_OUT_NATIVE ? g->w / 8 : (out_kind == SLP_OUT_F32 ? 4 : 8);
+    if ((uintptr_t)out % 128 != 0 || (ld_out * es) % 16 != 0 || ((T / J) * es) % 16 != 0) J = 1;
+  }
   if (J > 1) {
+    const bool pm = layout == SLP_POSITION_MAJOR;
     Segments seg;
-    int rc = make_segments(id, *g, states_in, ld, nstreams, T, J, st, seg);
+    int rc = make_segments(id, *g, states_in, ld, nstreams, T, J, st, seg, pm);
     if (rc != SLP_OK) return rc;
     FillParams q = p;
     q.sin = q.sout = seg.states;
     q.ld = q.nstreams = nstreams * J;
-    q.T = q.ld_out = T / J;
+    q.T = T / J;
+    if (pm) {
+      q.pm_n = nstreams;
+    } else if (ld_out == T) {
+      q.ld_out = T / J;
+    } else {
+      int sh = 0;
+      while ((1ull << sh) < J) ++sh;
+      q.jsh = (uint32_t)sh;
+    }
     rc = ops->fill(q, out_kind, layout, st);
     if (rc != SLP_OK || !states_out) return rc;
-    return segment_ends(*g, seg, nstreams, J, states_out, ld, st);
+    return segment_ends(*g, seg, nstreams, J, states_out, ld, st, pm ? 1 : 0);
   }
   return ops->fill(p, out_kind, layout, st);
 }

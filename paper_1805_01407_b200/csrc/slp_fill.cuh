@@ -119,6 +119,28 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t sr
                : "l"(reinterpret_cast<uint64_t>(map)), "r"(src), "r"(x), "r"(y), "r"(z)
                : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, uint32_t src, int x, int y, int z, int w) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+               :
+               : "l"(reinterpret_cast<uint64_t>(map)), "r"(src), "r"(x), "r"(y), "r"(z), "r"(w)
+               : "memory");
+}
+
+// element offset of stream-major row (segment) v: (v >> jsh) * ld_out + (v mod J) * T
+__device__ __forceinline__ uint64_t sm_row(const FillParams &p, uint64_t v) {
+  return (v >> p.jsh) * p.ld_out + (v & ((1ull << p.jsh) - 1)) * p.T;
+}
+// position-major segment v = j * pm_n + i: (row offset j * T, column i); no split: (0, v)
+__device__ __forceinline__ void pm_seg(const FillParams &p, uint64_t v, uint64_t &row_off, uint64_t &col) {
+  if (p.pm_n) {
+    const uint64_t j = v / p.pm_n;
+    row_off = j * p.T;
+    col = v - j * p.pm_n;
+  } else {
+    row_off = 0;
+    col = v;
+  }
+}
 
 // CSUM: also reduce the integer outputs while storing them (wrapping sum,
 // xor, exact sum and low-bit sum, as k_fused) -- "store mode plus fused
@@ -243,6 +265,8 @@ __global__ void __launch_bounds__(kFillThreads)
     const uint64_t row0 = u * 32;
     const uint64_t stream = row0 + lane;
     const bool valid = stream < p.nstreams;
+    uint64_t pm_roff = 0, pm_col = stream;  // position-major: this lane's segment (row offset, column)
+    if constexpr (MODE == FILL_POS || MODE == FILL_POS_TMA) pm_seg(p, stream, pm_roff, pm_col);
     word s[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) s[j] = nxt[j];
@@ -265,7 +289,7 @@ __global__ void __launch_bounds__(kFillThreads)
     for (uint64_t c = 0; c < nloop; ++c) {
       const uint64_t pos0 = c * CH;
       const uint32_t sub_end = (!TAIL_LOOP || c < ntiles) ? (uint32_t)CH : (uint32_t)(rem_loop / U) * U;
-      bits *const pos_row = out + pos0 * p.ld_out + stream;  // FILL_POS: row pos0, this lane's column
+      bits *const pos_row = out + (pm_roff + pos0) * p.ld_out + pm_col;  // FILL_POS: row pos0, this lane's column
       uint32_t tile = 0;
       auto wait_buffer = [&] {
         if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA || MODE == FILL_TMA_G) {
@@ -409,7 +433,8 @@ __global__ void __launch_bounds__(kFillThreads)
         fence_proxy_async_smem();
         __syncwarp();
         if (elect_one()) {
-          tma_store_3d(&tmap, tile, 0, (int)row0, (int)(pos0 * ES / 128));
+          tma_store_4d(&tmap, tile, 0, (int)(row0 & ((1ull << p.jsh) - 1)), (int)(row0 >> p.jsh),
+                       (int)(pos0 * ES / 128));
           bulk_commit();
         }
         ++issued;
@@ -417,7 +442,9 @@ __global__ void __launch_bounds__(kFillThreads)
         fence_proxy_async_smem();
         __syncwarp();
         if (elect_one()) {
-          tma_store_2d(&tmap, tile, (int)row0, (int)pos0);
+          uint64_t roff, col0;
+          pm_seg(p, row0, roff, col0);  // a warp's 32 segments share one row block (pm_n % 32 == 0)
+          tma_store_2d(&tmap, tile, (int)col0, (int)(roff + pos0));
           bulk_commit();
         }
         ++issued;
@@ -477,7 +504,7 @@ __global__ void __launch_bounds__(kFillThreads)
           cs_x ^= (uint64_t)r;
           cs_low += (uint32_t)r & (G::w == 64 ? 0x7FFu : 0xFFu);
         }
-        if (valid) out[(ntiles * CH + t) * p.ld_out + stream] = x;
+        if (valid) out[(pm_roff + ntiles * CH + t) * p.ld_out + pm_col] = x;
       }
     } else if constexpr (MODE == FILL_TMA_G) {
       // this row's last T - lead - ntiles*CH outputs (0 .. CH - 1 + lead_max):
@@ -586,7 +613,8 @@ __global__ void __launch_bounds__(kFillThreads)
             fence_proxy_async_smem();
             __syncwarp();
             if (elect_one()) {
-              tma_store_3d(&tmap, tile, 0, (int)row0, (int)(ntiles * CH * ES / 128));
+              tma_store_4d(&tmap, tile, 0, (int)(row0 & ((1ull << p.jsh) - 1)), (int)(row0 >> p.jsh),
+                           (int)(ntiles * CH * ES / 128));
               bulk_commit();
             }
             ++issued;  // only a committed store owns its buffer (bulk_wait_read counts groups)
@@ -608,7 +636,7 @@ __global__ void __launch_bounds__(kFillThreads)
             } else {
               asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
             }
-            out[grow * p.ld_out + ntiles * CH + col] = v;
+            out[sm_row(p, grow) + ntiles * CH + col] = v;
           }
         }
         __syncwarp();
@@ -657,7 +685,7 @@ __global__ void __launch_bounds__(kFillThreads)
           } else {
             asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
           }
-          out[grow * p.ld_out + ntiles * CH + col] = v;
+          out[sm_row(p, grow) + ntiles * CH + col] = v;
         }
       }
       __syncwarp();
@@ -733,7 +761,9 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pm2(FillParams p, const _
       fence_proxy_async_smem();
       __syncwarp();
       if (elect_one()) {
-        tma_store_2d(&tmap, tile, (int)row0, (int)(c * kPm2Pos));
+        uint64_t roff, col0;
+        pm_seg(p, row0, roff, col0);  // a warp's 64 segments share one row block (pm_n % 64 == 0)
+        tma_store_2d(&tmap, tile, (int)col0, (int)(roff + c * kPm2Pos));
         bulk_commit();
       }
       ++issued;
@@ -742,8 +772,11 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pm2(FillParams p, const _
       const bits xa = Cv::conv(eng.next_flat(a));
       const bits xb = Cv::conv(eng.next_flat(b));
       const uint64_t pos = ntiles * kPm2Pos + t;
-      if (vA) out[pos * p.ld_out + stA] = xa;
-      if (vB) out[pos * p.ld_out + stB] = xb;
+      uint64_t ra, ca, rb, cb;
+      pm_seg(p, stA, ra, ca);
+      pm_seg(p, stB, rb, cb);
+      if (vA) out[(ra + pos) * p.ld_out + ca] = xa;
+      if (vB) out[(rb + pos) * p.ld_out + cb] = xb;
     }
     if (sout) {
 #pragma unroll
@@ -760,7 +793,8 @@ template <class G, int OK>
 int launch_fill_pm2(const FillParams &p, cudaStream_t st) {
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof tmap);
-  int rc = make_store_tmap_pm(&tmap, p.out, 4, p.T, p.nstreams, p.ld_out, kPm2Pos, 64);
+  const uint64_t rows = p.pm_n ? p.T * (p.nstreams / p.pm_n) : p.T, cols = p.pm_n ? p.pm_n : p.nstreams;
+  int rc = make_store_tmap_pm(&tmap, p.out, 4, rows, cols, p.ld_out, kPm2Pos, 64);
   if (rc != SLP_OK) return rc;
   auto kern = k_fill_pm2<G, OK>;
   const int dev = current_device();
@@ -793,13 +827,14 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
   typename FillTmap<MODE>::type tmap;
   memset(&tmap, 0, sizeof tmap);
   if constexpr (MODE == FILL_TMA) {
-    int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, Shape::segs);
+    int rc = make_store_tmap(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, Shape::segs, (int)p.jsh);
     if (rc != SLP_OK) return rc;
   } else if constexpr (MODE == FILL_TMA_G) {
     int rc = make_store_tmap_group(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out, Shape::segs);
     if (rc != SLP_OK) return rc;
   } else if constexpr (MODE == FILL_POS_TMA) {
-    int rc = make_store_tmap_pm(&tmap, p.out, ES, p.T, p.nstreams, p.ld_out,
+    const uint64_t rows = p.pm_n ? p.T * (p.nstreams / p.pm_n) : p.T, cols = p.pm_n ? p.pm_n : p.nstreams;
+    int rc = make_store_tmap_pm(&tmap, p.out, ES, rows, cols, p.ld_out,
                                 Shape::row_bytes / ES);
     if (rc != SLP_OK) return rc;
   }
@@ -870,17 +905,23 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
   else
     return SLP_ERR_UNSUPPORTED;
   const int es = (ok == SLP_OUT_NATIVE) ? W / 8 : (ok == SLP_OUT_F32 ? 4 : 8);
+  // position-major segment split (pm_n > 0): the output is [pm_rows][ld_out];
+  // a TMA box covers one row block only when a warp's segments share it
+  const uint64_t pm_rows = p.pm_n ? p.T * (p.nstreams / p.pm_n) : p.T;
+  const uint64_t pm_cols = p.pm_n ? p.pm_n : p.nstreams;
   if constexpr (W == 32) {
     // position-major 4-byte outputs: two substreams per lane, 256-byte rows
-    if (layout == SLP_POSITION_MAJOR && es == 4 && tma_ok_pm(p.out, 4, p.T, p.nstreams, p.ld_out, kPm2Pos)) {
+    if (layout == SLP_POSITION_MAJOR && es == 4 && (!p.pm_n || p.pm_n % 64 == 0) &&
+        tma_ok_pm(p.out, 4, pm_rows, pm_cols, p.ld_out, kPm2Pos)) {
       if (ok == SLP_OUT_F32) return launch_fill_pm2<G, SLP_OUT_F32>(p, st);
       return launch_fill_pm2<G, SLP_OUT_NATIVE>(p, st);
     }
   }
   int mode;
   if (layout == SLP_POSITION_MAJOR)
-    mode = tma_ok_pm(p.out, es, p.T, p.nstreams, p.ld_out,
-                     fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs * 128 / es)
+    mode = (!p.pm_n || p.pm_n % 32 == 0) &&
+                   tma_ok_pm(p.out, es, pm_rows, pm_cols, p.ld_out,
+                             fill_cfg(G::id, ok == SLP_OUT_NATIVE ? FILL_KIND_NATIVE : FILL_KIND_CONVERT).segs * 128 / es)
                ? FILL_POS_TMA
                : FILL_POS;
   else if (layout != SLP_STREAM_MAJOR)
@@ -894,6 +935,8 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
     mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, ssegs)
                ? FILL_TMA
                : (tma_group_ok(p.out, es, p.T, p.nstreams, p.ld_out, ssegs) ? FILL_TMA_G : FILL_STAGED);
+    // stream-major segment rows (jsh > 0) are addressed through the 4-D store map only
+    if (p.jsh && (mode != FILL_TMA || short_rows)) return SLP_ERR_UNSUPPORTED;
   }
 #define SLP_FILL_CASE(OKV)                                                                              \
   if (ok == OKV) {                                                                                      \

@@ -31,6 +31,14 @@ struct FillParams {
   void *partials;           // store+checksum mode: slp_checksum[grid]
   size_t workspace_bytes;
   GenRt rt;                // run-time generator parameters (custom engines)
+  // segment split (slp_fill for few, long substreams): the nstreams rows are
+  // segments of n = nstreams >> jsh real substreams, T outputs each.
+  // Stream-major: segment v = i * J + j (J = 1 << jsh) is row i, columns
+  // [j * T, (j + 1) * T): element offset (v >> jsh) * ld_out + (v & (J - 1)) * T.
+  // Position-major (pm_n = n > 0): segment v = j * n + i is column i, rows
+  // [j * T, (j + 1) * T).  jsh = 0 and pm_n = 0: no split.
+  uint32_t jsh;
+  uint64_t pm_n;
 };
 
 struct FusedParams {
@@ -137,7 +145,8 @@ int fill_grid_mult();
 int cuda_fail(const char *what);
 int check_launch(const char *what);
 bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);
-int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);
+int make_store_tmap(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs,
+                    int jsh = 0);
 bool tma_ok_pm(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int ch);
 int make_store_tmap_pm(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int ch,
                        int box_rows = 32);

@@ -162,12 +162,16 @@ def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor
     return out
 
 
-def _split_factor(spec: GeneratorSpec, n: int, T: int, layout: str, ld_out: int) -> int:
+def _split_factor(spec: GeneratorSpec, n: int, T: int, layout: str, ld_out: int, es: int | None = None) -> int:
     """Segments per substream the C ABI uses internally for few, long
-    substreams (slp_split_factor; stream-major contiguous rows only)."""
-    if layout != "stream" or ld_out != T:
-        return 1
-    return int(_native.lib().slp_split_factor(native_id(spec), n, T))
+    substreams (slp_split_factor): contiguous and padded stream-major rows
+    (padded: 16-byte row pitch and segment length) and position-major."""
+    J = int(_native.lib().slp_split_factor(native_id(spec), n, T))
+    if J > 1 and layout == "stream" and ld_out != T:
+        es = es or spec.kind.w // 8
+        if (ld_out * es) % 16 or ((T // J) * es) % 16:
+            return 1
+    return J
 
 
 _ws_bytes: dict = {}
