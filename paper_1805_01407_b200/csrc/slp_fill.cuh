@@ -1,6 +1,8 @@
 // Kernels K2/K3: step + scramble + convert + store (k_fill) and its launchers.
 #pragma once
 
+#include <cstdlib>
+
 #include "slp_gen.cuh"
 
 namespace slp {
@@ -814,6 +816,159 @@ int launch_fill_pm2(const FillParams &p, cudaStream_t st) {
   return check_launch("k_fill_pm2");
 }
 
+// Position-major rows that no TMA tensor map can address (odd pitch for
+// 8-byte outputs, pitch % 4 != 0 for 4-byte outputs, unaligned base): with
+// one coalesced warp store per output, every warp's 32-element row piece
+// starts and ends inside a 32-byte sector, and each such partial-sector write
+// costs a DRAM read-modify-write (ncu: 0.90 GB of DRAM reads per 8 GiB
+// fill, 2.4 TB/s; profiles/round2_pm_odd_ncu.csv).  Here the CTA's 7 warps
+// (224 consecutive substreams) stage CH positions in shared memory, each
+// row laid out at the same offset modulo 16 as in global memory; then one
+// thread writes the 32-byte-aligned interior of every row with a 1-D bulk
+// copy (cp.async.bulk.global.shared::cta: whole sectors only) and a few
+// threads store the 0-3 edge elements at each end.  Partial sectors remain
+// only at CTA boundaries (2 per 224 outputs instead of 2 per 32).
+constexpr int kPosCtaCH = 32;  // positions per tile
+
+template <int ES>
+struct PosCta {
+  static constexpr int W = kFillWarps * 32;                  // substreams per CTA
+  static constexpr int ROW = ((W * ES + 32 + 127) / 128) * 128;  // smem bytes per row (+ offset room)
+  static constexpr int TILE = kPosCtaCH * ROW;
+  static constexpr int SMEM = 2 * TILE + 128;
+};
+
+template <class G, int OK>
+__global__ void __launch_bounds__(kFillThreads) k_fill_pos_cta(FillParams p) {
+  const G eng = G::load(p.rt);
+  using word = typename G::word;
+  using Cv = Out<OK, word>;
+  using bits = typename Cv::bits;
+  constexpr int K = G::k;
+  constexpr int ES = sizeof(bits);
+  using PC = PosCta<ES>;
+  constexpr int CH = kPosCtaCH;
+  static_assert(CH % K == 0, "tiles must cover whole ring periods");
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
+  uint8_t *sgen = smem_raw + (sbase - smem_u32(smem_raw));  // generic pointer of sbase
+  const int tid = threadIdx.x;
+  const word *__restrict__ sin = static_cast<const word *>(p.sin);
+  word *sout = static_cast<word *>(p.sout);
+  bits *__restrict__ out = static_cast<bits *>(p.out);
+  const uint64_t nblk = (p.nstreams + PC::W - 1) / PC::W;
+  const uint64_t ntiles = (p.T + CH - 1) / CH;
+  uint32_t issued = 0;
+  for (uint64_t cb = blockIdx.x; cb < nblk; cb += gridDim.x) {
+    const uint64_t c0 = cb * PC::W;
+    const uint64_t stream = c0 + tid;
+    const bool valid = stream < p.nstreams;
+    const int wcols = (int)(p.nstreams - c0 < (uint64_t)PC::W ? p.nstreams - c0 : PC::W);
+    word s[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) s[j] = valid ? sin[j * p.ld + stream] : (word)0;
+    for (uint64_t c = 0; c < ntiles; ++c) {
+      const uint64_t pos0 = c * CH;
+      const int rows = (int)(p.T - pos0 < (uint64_t)CH ? p.T - pos0 : CH);
+      const uint32_t buf = (issued & 1) * PC::TILE;
+      // the bulk stores of the tile two back must have read this buffer
+      if (issued >= 2 && tid == 0) bulk_wait_read<1>();
+      __syncthreads();
+      if (rows == CH) {
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+          const bits x = Cv::conv(eng.output(s, t % K));
+          eng.step(s, t % K);
+          const uint64_t gaddr = (uint64_t)(out + (pos0 + t) * p.ld_out + c0);
+          const uint32_t a = buf + t * PC::ROW + (uint32_t)(gaddr & 15) + tid * ES;
+          if constexpr (ES == 8)
+            asm volatile("st.shared.b64 [%0], %1;" ::"r"(sbase + a), "l"((uint64_t)x) : "memory");
+          else
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sbase + a), "r"((uint32_t)x) : "memory");
+        }
+      } else {
+        for (int t = 0; t < rows; ++t) {  // last, partial tile: scalar steps keep flat order
+          const bits x = Cv::conv(eng.next_flat(s));
+          const uint64_t gaddr = (uint64_t)(out + (pos0 + t) * p.ld_out + c0);
+          const uint32_t a = buf + t * PC::ROW + (uint32_t)(gaddr & 15) + tid * ES;
+          if constexpr (ES == 8)
+            asm volatile("st.shared.b64 [%0], %1;" ::"r"(sbase + a), "l"((uint64_t)x) : "memory");
+          else
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sbase + a), "r"((uint32_t)x) : "memory");
+        }
+      }
+      fence_proxy_async_smem();
+      __syncthreads();
+      // row t: global bytes [g0, g1); interior [A, B) = whole 32-byte sectors
+      if (tid == 0) {
+        for (int t = 0; t < rows; ++t) {
+          const uint64_t g0 = (uint64_t)(out + (pos0 + t) * p.ld_out + c0), g1 = g0 + (uint64_t)wcols * ES;
+          const uint64_t A = (g0 + 31) & ~31ull, B = g1 & ~31ull;
+          if (B > A) {
+            const uint32_t src = sbase + buf + t * PC::ROW + (uint32_t)(g0 & 15) + (uint32_t)(A - g0);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(A), "r"(src),
+                         "r"((uint32_t)(B - A))
+                         : "memory");
+          }
+        }
+        bulk_commit();
+      }
+      // edges: elements outside [A, B), at most 3 (7 for 4-byte outputs) per end and row
+      constexpr int EPS = 32 / ES;  // elements per sector
+      for (int q = tid; q < rows * 2 * EPS; q += kFillThreads) {
+        const int t = q / (2 * EPS), r = q % (2 * EPS);
+        const uint64_t g0 = (uint64_t)(out + (pos0 + t) * p.ld_out + c0), g1 = g0 + (uint64_t)wcols * ES;
+        const uint64_t A = (g0 + 31) & ~31ull, B = g1 & ~31ull;
+        // head: elements before A; tail: elements from B on (without an
+        // interior, B <= A, the piece is shorter than 64 bytes: head and tail
+        // together cover its < 2 * EPS elements)
+        int e;
+        if (r < EPS) {
+          e = r;
+          if (B > A && g0 + (uint64_t)e * ES >= A) continue;
+        } else {
+          e = (B > A ? (int)((B - g0) / ES) : EPS) + (r - EPS);
+        }
+        if (e >= wcols) continue;
+        const uint32_t a = sbase + buf + t * PC::ROW + (uint32_t)(g0 & 15) + e * ES;
+        bits v;
+        if constexpr (ES == 8)
+          asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+        else
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+        out[(pos0 + t) * p.ld_out + c0 + e] = v;
+      }
+      ++issued;
+    }
+    if (valid && sout) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) sout[j * p.ld + stream] = s[j];
+    }
+  }
+  if (tid == 0) bulk_wait_all<0>();
+}
+
+template <class G, int OK>
+int launch_fill_pos_cta(const FillParams &p, cudaStream_t st) {
+  using bits = typename Out<OK, typename G::word>::bits;
+  using PC = PosCta<(int)sizeof(bits)>;
+  auto kern = k_fill_pos_cta<G, OK>;
+  const int dev = current_device();
+  static std::atomic<int> attr_set[64];
+  if (dev < 0 || dev >= 64) return SLP_ERR_CUDA;
+  if (!attr_set[dev]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PC::SMEM) != cudaSuccess)
+      return cuda_fail("cudaFuncSetAttribute(pos_cta)");
+    attr_set[dev] = 1;
+  }
+  const uint64_t nblk = (p.nstreams + PC::W - 1) / PC::W;
+  if (nblk == 0 || p.T == 0) return SLP_OK;
+  const uint64_t cap = (uint64_t)sm_count(dev) * fill_grid_mult();
+  const unsigned grid = (unsigned)(nblk < cap ? nblk : cap);
+  kern<<<grid, kFillThreads, PC::SMEM, st>>>(p);
+  return check_launch("k_fill_pos_cta");
+}
+
 template <class G, int OK, int MODE, bool CSUM = false, bool SHORT = false, bool TAIL = false>
 int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) {
   using Shape = FillShape<G, SHORT ? (int)FILL_KIND_SHORT : fill_kind<OK, CSUM>()>;
@@ -937,6 +1092,18 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
                : (tma_group_ok(p.out, es, p.T, p.nstreams, p.ld_out, ssegs) ? FILL_TMA_G : FILL_STAGED);
     // stream-major segment rows (jsh > 0) are addressed through the 4-D store map only
     if (p.jsh && (mode != FILL_TMA || short_rows)) return SLP_ERR_UNSUPPORTED;
+  }
+  // rows no TMA map can address: the CTA-staged sector-aligned path (no split)
+  static const bool pos_cta_off = std::getenv("SLP_POS_CTA_OFF") != nullptr;  // A/B: element stores
+  if (mode == FILL_POS && !p.pm_n && ((uintptr_t)p.out % es) == 0 && !pos_cta_off) {
+    if constexpr (W == 64) {
+      if (ok == SLP_OUT_F64) return launch_fill_pos_cta<G, SLP_OUT_F64>(p, st);
+      return launch_fill_pos_cta<G, SLP_OUT_NATIVE>(p, st);
+    } else {
+      if (ok == SLP_OUT_F32) return launch_fill_pos_cta<G, SLP_OUT_F32>(p, st);
+      if (ok == SLP_OUT_U64) return launch_fill_pos_cta<G, SLP_OUT_U64>(p, st);
+      return launch_fill_pos_cta<G, SLP_OUT_NATIVE>(p, st);
+    }
   }
 #define SLP_FILL_CASE(OKV)                                                                              \
   if (ok == OKV) {                                                                                      \

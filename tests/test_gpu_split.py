@@ -89,3 +89,43 @@ def test_split_rates_lift_the_cliff():
         e1.synchronize()
         tbs = 16 * T * 8 * 3 / (e0.elapsed_time(e1) / 1e3) / 1e12
         assert tbs > 0.5, (args.get("layout", "stream"), tbs)
+
+
+@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro128plus", "xoroshiro1024starstar",
+                                  "xoshiro128starstar", "xoroshiro64starstar"])
+@pytest.mark.parametrize("n,T,pad,off", [(225, 70, 0, 0), (1001, 64, 2, 1), (449, 33, 1, 3), (3, 100, 0, 1),
+                                         (672, 96, 5, 2), (7, 5, 0, 0)])
+@pytest.mark.parametrize("kind", ["native", "float", "u64"])
+def test_position_major_unaligned_rows(name, n, T, pad, off, kind):
+    """Rows no TMA map can address (odd pitch / unaligned base): the
+    CTA-staged path (k_fill_pos_cta: sector-aligned bulk interiors, element
+    stores at the CTA edges) -- partial CTA blocks, partial tiles, padding."""
+    spec = P.get_spec(name)
+    w = spec.kind.w
+    if kind == "u64" and w == 64:
+        pytest.skip("u64 is native for w = 64")
+    k = ("f64" if w == 64 else "f32") if kind == "float" else kind
+    dt = {("native", 64): torch.uint64, ("native", 32): torch.uint32, ("f64", 64): torch.float64,
+          ("f32", 32): torch.float32, ("u64", 32): torch.uint64}[(k, w)]
+    sub = D.Substreams.from_seed(spec, 9, n)
+    S0 = sub.states_numpy()
+    ld = n + pad + (1 if (n + pad) % 2 == 0 else 0)  # odd pitch
+    flat = torch.empty(T * ld + off + 8, dtype=dt, device="cuda")
+    flat.view(torch.uint8).fill_(SENT)
+    view = flat[off:off + T * ld].view(T, ld)[:, :n]
+    sub.fill(T, out=view, layout="position", kind=k)
+    want, want_S = want_outputs(name, S0, T)
+    if k == "f64":
+        want = O.to_f64(want)
+    elif k == "f32":
+        want = O.to_f32(want)
+    got = flat.cpu().numpy()
+    body = got[off:off + T * ld].reshape(T, ld)
+    np.testing.assert_array_equal(body[:, :n].view(np.uint8), np.ascontiguousarray(want.T.astype(got.dtype)).view(np.uint8))
+    mask = np.ones(got.shape, dtype=bool)
+    mask[off:off + T * ld] = False
+    inner = np.zeros((T, ld), dtype=bool)
+    inner[:, :n] = True
+    mask[off:off + T * ld] |= ~inner.reshape(-1)
+    assert (got[mask].view(np.uint8) == SENT).all()  # nothing outside the view written
+    np.testing.assert_array_equal(sub.states_numpy().astype(np.uint64), want_S)
