@@ -828,7 +828,7 @@ int launch_fill_pm2(const FillParams &p, cudaStream_t st) {
 // copy (cp.async.bulk.global.shared::cta: whole sectors only) and a few
 // threads store the 0-3 edge elements at each end.  Partial sectors remain
 // only at CTA boundaries (2 per 224 outputs instead of 2 per 32).
-constexpr int kPosCtaCH = 32;  // positions per tile
+constexpr int kPosCtaCH = 16;  // positions per tile (2 x 30 KB buffers: 3 CTAs per SM overlap their phases)
 
 template <int ES>
 struct PosCta {
@@ -871,16 +871,20 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pos_cta(FillParams p) {
       const uint64_t pos0 = c * CH;
       const int rows = (int)(p.T - pos0 < (uint64_t)CH ? p.T - pos0 : CH);
       const uint32_t buf = (issued & 1) * PC::TILE;
-      // the bulk stores of the tile two back must have read this buffer
-      if (issued >= 2 && tid == 0) bulk_wait_read<1>();
+      // the bulk stores of the tile two back (issued by lane 0 of every warp)
+      // must have read this buffer
+      if (issued >= 2 && (tid & 31) == 0) bulk_wait_read<1>();
       __syncthreads();
+      // row t of the tile starts at global byte g_row0 + t * pitch; in shared
+      // memory at the same offset modulo 16
+      const uint64_t pitch = p.ld_out * ES;
+      const uint64_t g_row0 = (uint64_t)(out + pos0 * p.ld_out + c0);
       if (rows == CH) {
 #pragma unroll
         for (int t = 0; t < CH; ++t) {
           const bits x = Cv::conv(eng.output(s, t % K));
           eng.step(s, t % K);
-          const uint64_t gaddr = (uint64_t)(out + (pos0 + t) * p.ld_out + c0);
-          const uint32_t a = buf + t * PC::ROW + (uint32_t)(gaddr & 15) + tid * ES;
+          const uint32_t a = buf + t * PC::ROW + (uint32_t)((g_row0 + t * pitch) & 15) + tid * ES;
           if constexpr (ES == 8)
             asm volatile("st.shared.b64 [%0], %1;" ::"r"(sbase + a), "l"((uint64_t)x) : "memory");
           else
@@ -889,8 +893,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pos_cta(FillParams p) {
       } else {
         for (int t = 0; t < rows; ++t) {  // last, partial tile: scalar steps keep flat order
           const bits x = Cv::conv(eng.next_flat(s));
-          const uint64_t gaddr = (uint64_t)(out + (pos0 + t) * p.ld_out + c0);
-          const uint32_t a = buf + t * PC::ROW + (uint32_t)(gaddr & 15) + tid * ES;
+          const uint32_t a = buf + t * PC::ROW + (uint32_t)((g_row0 + t * pitch) & 15) + tid * ES;
           if constexpr (ES == 8)
             asm volatile("st.shared.b64 [%0], %1;" ::"r"(sbase + a), "l"((uint64_t)x) : "memory");
           else
@@ -899,10 +902,11 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pos_cta(FillParams p) {
       }
       fence_proxy_async_smem();
       __syncthreads();
-      // row t: global bytes [g0, g1); interior [A, B) = whole 32-byte sectors
-      if (tid == 0) {
-        for (int t = 0; t < rows; ++t) {
-          const uint64_t g0 = (uint64_t)(out + (pos0 + t) * p.ld_out + c0), g1 = g0 + (uint64_t)wcols * ES;
+      // row t: global bytes [g0, g1); interior [A, B) = whole 32-byte sectors;
+      // lane 0 of warp w issues the rows t = w mod kFillWarps
+      if ((tid & 31) == 0) {
+        for (int t = tid >> 5; t < rows; t += kFillWarps) {
+          const uint64_t g0 = g_row0 + t * pitch, g1 = g0 + (uint64_t)wcols * ES;
           const uint64_t A = (g0 + 31) & ~31ull, B = g1 & ~31ull;
           if (B > A) {
             const uint32_t src = sbase + buf + t * PC::ROW + (uint32_t)(g0 & 15) + (uint32_t)(A - g0);
@@ -917,7 +921,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pos_cta(FillParams p) {
       constexpr int EPS = 32 / ES;  // elements per sector
       for (int q = tid; q < rows * 2 * EPS; q += kFillThreads) {
         const int t = q / (2 * EPS), r = q % (2 * EPS);
-        const uint64_t g0 = (uint64_t)(out + (pos0 + t) * p.ld_out + c0), g1 = g0 + (uint64_t)wcols * ES;
+        const uint64_t g0 = g_row0 + t * pitch, g1 = g0 + (uint64_t)wcols * ES;
         const uint64_t A = (g0 + 31) & ~31ull, B = g1 & ~31ull;
         // head: elements before A; tail: elements from B on (without an
         // interior, B <= A, the piece is shorter than 64 bytes: head and tail
@@ -945,7 +949,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pos_cta(FillParams p) {
       for (int j = 0; j < K; ++j) sout[j * p.ld + stream] = s[j];
     }
   }
-  if (tid == 0) bulk_wait_all<0>();
+  if ((tid & 31) == 0) bulk_wait_all<0>();
 }
 
 template <class G, int OK>
@@ -954,16 +958,19 @@ int launch_fill_pos_cta(const FillParams &p, cudaStream_t st) {
   using PC = PosCta<(int)sizeof(bits)>;
   auto kern = k_fill_pos_cta<G, OK>;
   const int dev = current_device();
-  static std::atomic<int> attr_set[64];
+  static std::atomic<int> per_sm[64];
   if (dev < 0 || dev >= 64) return SLP_ERR_CUDA;
-  if (!attr_set[dev]) {
+  if (!per_sm[dev]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PC::SMEM) != cudaSuccess)
       return cuda_fail("cudaFuncSetAttribute(pos_cta)");
-    attr_set[dev] = 1;
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kFillThreads, PC::SMEM) != cudaSuccess || b < 1)
+      return cuda_fail("occupancy(pos_cta)");
+    per_sm[dev] = b;
   }
   const uint64_t nblk = (p.nstreams + PC::W - 1) / PC::W;
   if (nblk == 0 || p.T == 0) return SLP_OK;
-  const uint64_t cap = (uint64_t)sm_count(dev) * fill_grid_mult();
+  const uint64_t cap = (uint64_t)sm_count(dev) * per_sm[dev] * fill_grid_mult();
   const unsigned grid = (unsigned)(nblk < cap ? nblk : cap);
   kern<<<grid, kFillThreads, PC::SMEM, st>>>(p);
   return check_launch("k_fill_pos_cta");
