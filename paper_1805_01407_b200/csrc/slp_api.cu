@@ -555,9 +555,12 @@ static int poly_table_on_device(int id, int dev, const uint64_t *poly, cudaStrea
 constexpr uint64_t kJumpTableMinStates = 65536;
 
 static bool use_jump_tables(uint64_t count) {
-  const char *v = std::getenv("SLP_INIT_TABLES");
-  if (v && *v == '0') return false;
-  return count >= 16384;
+  static const long min_states = [] {  // SLP_INIT_TABLES=0 disables K1t; =N sets the threshold (A/B)
+    const char *v = std::getenv("SLP_INIT_TABLES");
+    if (v && *v == '0') return -1L;
+    return v && *v ? std::atol(v) : 16384L;
+  }();
+  return min_states >= 0 && count >= (uint64_t)min_states;
 }
 
 }  // namespace slp

@@ -12,6 +12,7 @@
 #include <immintrin.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -549,6 +550,17 @@ void host_jump(const GenDesc &g, const Poly &p, uint64_t *flat) {
 // by exactly one polynomial jump, as in the reference.
 
 static constexpr uint64_t kDirect = 1024;
+
+// direct (launch-0) polynomials per plan: fewer for wide engines, whose
+// non-uniform direct jumps are latency-bound (SLP_PLAN_DIRECT overrides, A/B)
+static uint64_t plan_direct(int nbits) {
+  static const long env = [] {
+    const char *v = std::getenv("SLP_PLAN_DIRECT");
+    return v && *v ? std::atol(v) : 0L;
+  }();
+  if (env > 0) return (uint64_t)env;
+  return nbits <= 256 ? kDirect : (nbits <= 512 ? kDirect / 4 : kDirect / 8);
+}
 static constexpr uint64_t kRadix = 8;
 
 struct PlanKey {
@@ -581,7 +593,7 @@ std::shared_ptr<const InitPlan> init_plan(int id, const uint64_t *steps, int ste
   // caller with many different counts (HWD ranges) shares O(log n) plans and
   // their device tables instead of one per count.
   const GenDesc &gd = *gen_desc(eid);
-  const uint64_t nd = gd.n() <= 256 ? kDirect : (gd.n() <= 512 ? kDirect / 4 : kDirect / 8);
+  const uint64_t nd = plan_direct(gd.n());
   uint64_t n = nd;
   while (n < n_req) n *= kRadix;
   PlanKey key{eid, st, n};
@@ -605,7 +617,7 @@ std::shared_ptr<const InitPlan> init_plan(int id, const uint64_t *steps, int ste
   const Reducer red(P);
   // fewer direct polynomials for wide engines: each costs a host mulmod of
   // degree-n polys (plan build time), the rounds that replace them are cheap
-  const uint64_t ndirect = g.n() <= 256 ? kDirect : (g.n() <= 512 ? kDirect / 4 : kDirect / 8);
+  const uint64_t ndirect = plan_direct(g.n());
   const uint64_t m0 = n < ndirect ? n : ndirect;
   // launch 0: x^(iJ) for i < m0
   Poly cur{1};
