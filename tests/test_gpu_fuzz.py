@@ -180,3 +180,96 @@ def test_split_fuzz(seed):
         _, c2 = D.fill_checksum(spec, sub2.states, T)
         assert (c2.sum, c2.xor, c2.mant) == (oc["sum"], oc["xor"], oc["mant"]), msg
         np.testing.assert_array_equal(sub2.states.cpu().numpy().astype(np.uint64), want_S, err_msg=msg)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SLP_FUZZ_SEEDS", "12")) // 2 + 1))
+def test_few_long_split_fuzz(seed):
+    """Few, long substreams through the segment split, in every layout the
+    split serves: contiguous and padded stream-major rows, position-major
+    (incl. unaligned pitch, which falls back to the unsplit paths)."""
+    rng = np.random.default_rng(13000 + seed)
+    for _ in range(4):
+        name = ALL[rng.integers(len(ALL))]
+        spec = P.get_spec(name)
+        w = spec.kind.w
+        n = int(rng.choice([1, 2, 5, 16, 33]))
+        T = int(rng.choice([1 << 13, 3 << 12, 1 << 14, 5 << 12]))
+        layout = str(rng.choice(["stream", "position"]))
+        pad = int(rng.choice([0, 1, 2, 8, 16]))
+        flat = rng.integers(0, 1 << 63, size=(spec.kind.k, n), dtype=np.uint64) | np.uint64(1)
+        if w == 32:
+            flat &= np.uint64(0xFFFFFFFF)
+        want, want_S = O.vec_outputs(name, flat, T)
+        want = want.astype(np.uint64 if w == 64 else np.uint32)
+        if layout == "position":
+            want = want.T.copy()
+        rows, cols = want.shape
+        dt = torch.uint64 if w == 64 else torch.uint32
+        big = torch.zeros((rows, cols + pad), dtype=dt, device="cuda")
+        sub = D.Substreams.from_states(spec, flat)
+        D.fill(spec, sub.states, T, out=big[:, :cols], layout=layout)
+        msg = f"{name} n={n} T={T} {layout} pad={pad} J={D._split_factor(spec, n, T, layout, cols + pad)}"
+        got = big.cpu().numpy()
+        np.testing.assert_array_equal(got[:, :cols], want, err_msg=msg)
+        assert not got[:, cols:].any(), msg
+        np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S, err_msg=msg)
+
+
+_SHAPES = [("xoroshiro", 2, 64), ("xoroshiro", 16, 64), ("xoshiro", 4, 64), ("xoshiro", 8, 64),
+           ("xorshift", 2, 64), ("xoroshiro", 2, 32), ("xoshiro", 4, 32), ("xoshiro", 8, 32), ("xorshift", 2, 32)]
+
+
+def _random_custom(rng, tag):
+    fam, k, w = _SHAPES[rng.integers(len(_SHAPES))]
+    a, b, c = (int(x) for x in rng.integers(1, w, size=3))
+    kind = str(rng.choice(["none", "plus", "star", "plusplus", "starstar"]))
+    words = [0, k - 1] if (fam == "xoroshiro" and k > 2) else list(range(k))
+    i, j = int(rng.choice(words)), int(rng.choice(words))
+    odd = lambda: int(rng.integers(1, 1 << (w - 1))) * 2 + 1  # noqa: E731
+    kw = {"none": dict(word_i=i), "plus": dict(word_i=i, word_j=j), "star": dict(word_i=i, S=odd()),
+          "plusplus": dict(word_i=i, word_j=j, R=int(rng.integers(1, w))),
+          "starstar": dict(word_i=i, S=odd(), R=int(rng.integers(1, w)), T=odd())}[kind]
+    name = f"fuzz-{tag}"
+    spec = P.custom_spec(fam, k, w, a, b, c if fam != "xoshiro" else None,
+                         scrambler=P.ScramblerSpec(kind, **kw), name=name)
+    sc = spec.scrambler
+    O.SPECS[name] = (fam, k, w, (a, b, c if fam != "xoshiro" else None), kind, sc.word_i, sc.word_j, sc.S, sc.R,
+                     sc.T)
+    return name, spec
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SLP_FUZZ_SEEDS", "12")) // 2 + 1))
+def test_custom_engine_fuzz(seed):
+    """Random custom_spec engines (any parameters, scrambler and word choice)
+    through the run-time parameter kernels: fill (both layouts, all kinds)
+    and the fused checksum against the oracle."""
+    rng = np.random.default_rng(17000 + seed)
+    for it in range(4):
+        name, spec = _random_custom(rng, f"{seed}-{it}")
+        w = spec.kind.w
+        n = int(rng.choice([1, 33, 300, 2000]))
+        T = int(rng.choice([1, 17, 64, 129, 512, 1000]))
+        layout = str(rng.choice(["stream", "position"]))
+        kinds = ["native", "f64"] if w == 64 else ["native", "u64", "f32"]
+        kind = kinds[rng.integers(len(kinds))]
+        flat = rng.integers(0, 1 << 63, size=(spec.kind.k, n), dtype=np.uint64) | np.uint64(1)
+        if w == 32:
+            flat &= np.uint64(0xFFFFFFFF)
+        want, want_S = O.vec_outputs(name, flat, T)
+        oc = O.checksum(want, w)
+        want = want.astype(np.uint64 if w == 64 else np.uint32)
+        if kind == "u64":
+            want = want.astype(np.uint64)
+        elif kind == "f64":
+            want = O.to_f64(want)
+        elif kind == "f32":
+            want = O.to_f32(want)
+        if layout == "position":
+            want = want.T.copy()
+        msg = f"{spec} n={n} T={T} {layout} {kind}"
+        sub = D.Substreams.from_states(spec, flat)
+        got = D.fill(spec, sub.states, T, kind=kind, layout=layout).cpu().numpy()
+        np.testing.assert_array_equal(got.view(np.uint8), want.view(np.uint8), err_msg=msg)
+        np.testing.assert_array_equal(sub.states.cpu().numpy().astype(np.uint64), want_S, err_msg=msg)
+        c = D.Substreams.from_states(spec, flat).checksum(T, exact=True)
+        assert (c.sum, c.xor, c.mant) == (oc["sum"], oc["xor"], oc["mant"]), msg
