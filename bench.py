@@ -368,14 +368,19 @@ def run_ours(args):
     e2e_os = None
     if args.e2e_steps > 0:
         total = 1 << 30
-        it = P.output_stream(spec, SEED, total, lanes=1 << 16, lane_len=1024)
-        got = next(it).size  # warm: plans, staging buffers
+        # warm-up stream: init plans and the process's pool of page-locked
+        # chunk buffers (pinning 3 x 512 MB once per process)
+        for c in P.output_stream(spec, SEED + 1, 1 << 28, lanes=1 << 16, lane_len=1024):
+            pass  # a consumer holding one chunk while the next is produced: 3 buffers
         t_os = time.perf_counter()
-        for c in it:
+        got = 0
+        for c in P.output_stream(spec, SEED, total, lanes=1 << 16, lane_len=1024):
             got += c.size
         dt_os = time.perf_counter() - t_os
-        e2e_os = {"value": (got - (1 << 26)) / dt_os, "unit": "values/s",
-                  "api": "output_stream(spec, 42, 2^30, lanes=2^16, lane_len=1024): fresh numpy uint64 chunks",
+        del c
+        e2e_os = {"value": got / dt_os, "unit": "values/s",
+                  "api": "output_stream(spec, 42, 2^30, lanes=2^16, lane_len=1024) from the seed: numpy uint64 "
+                         "chunks owned by the caller (DMA into pooled page-locked buffers, recycled when dropped)",
                   "wall_s": round(dt_os, 3)}
 
     extra = {}
