@@ -360,6 +360,13 @@ size_t cache_budget() {
   return b;
 }
 
+// a stream being captured into a CUDA graph: waits on and records of events
+// that live outside the graph must be external nodes
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive;
+}
+
 // with g_cache_mu held: the entry, pinned and waited on by `st`, or nullptr
 DevEntry *cache_find(const DevKey &key, cudaStream_t st) {
   auto it = g_cache.find(key);
@@ -367,7 +374,7 @@ DevEntry *cache_find(const DevKey &key, cudaStream_t st) {
   DevEntry *e = it->second.get();
   e->tick = ++g_cache_tick;
   ++e->pins;
-  if (e->ready) cudaStreamWaitEvent(st, e->ready, 0);
+  if (e->ready) cudaStreamWaitEvent(st, e->ready, capturing(st) ? cudaEventWaitExternal : 0);
   return e;
 }
 
@@ -416,7 +423,7 @@ void cache_unpin(DevEntry *e, cudaStream_t st) {
   for (auto &u : e->uses)
     if (u.first == st) ev = u.second;
   if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) e->uses.emplace_back(st, ev);
-  if (ev) cudaEventRecord(ev, st);
+  if (ev) cudaEventRecordWithFlags(ev, st, capturing(st) ? cudaEventRecordExternal : cudaEventRecordDefault);
   --e->pins;
 }
 

@@ -61,3 +61,42 @@ def test_bounded_cache_evicts_safely():
     r = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "ok" in r.stdout
+
+
+def test_fill_is_capturable_in_a_cuda_graph():
+    """Once its plan is warm, a fill -- including the segment split (K1 jumps,
+    stream-ordered scratch, K2, segment ends) -- does no host synchronisation
+    and can be captured in a CUDA graph and replayed."""
+    import numpy as np
+    import torch
+
+    import paper_1805_01407_b200 as P
+    from paper_1805_01407_b200 import device as D
+    from oracle import oracle as O
+
+    for name, n, T in (("xoshiro256starstar", 4, 1 << 15), ("xoroshiro128plus", 5000, 256)):
+        spec = P.get_spec(name)
+        S0 = D.Substreams.from_seed(spec, 21, n).states_numpy().astype(np.uint64)
+        states = D.Substreams.from_states(spec, S0).states
+        out = torch.empty((n, T), dtype=torch.uint64, device="cuda")
+        D.fill(spec, states.clone(), T, out=out)  # warm: plan, jump tables, pool
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            states.copy_(torch.from_numpy(S0).cuda())
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                D.fill(spec, states, T, out=out)
+        torch.cuda.synchronize()
+        want1, S1 = O.vec_outputs(name, S0, T)
+        want2, S2 = O.vec_outputs(name, S1, T)
+        states.copy_(torch.from_numpy(S0).cuda())
+        g.replay()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy(), want1)
+        g.replay()  # states advanced in place by the first replay
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy(), want2)
+        np.testing.assert_array_equal(states.cpu().numpy().astype(np.uint64), S2)
