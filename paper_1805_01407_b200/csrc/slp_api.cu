@@ -227,7 +227,7 @@ bool tma_group_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64
   const uint64_t seg = 128 / es;
   const uint64_t g = row_group(ld_out * es, es);
   return ((uintptr_t)out % es) == 0 && T >= (uint64_t)segs * seg + row_align(es) / es && ld_out >= T && nstreams >= g &&
-         g <= 8 &&
+         g <= 4 &&  // k_fill's tile addressing needs 32 / g rows per piece to be a multiple of 8
          T < (1ull << 31) && g * ld_out * es < (1ull << 40) && nstreams < (1ull << 31);
 }
 

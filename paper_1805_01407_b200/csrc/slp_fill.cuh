@@ -227,6 +227,16 @@ __global__ void __launch_bounds__(kFillThreads)
   };
   int lead = 0;  // FILL_TMA_G: outputs of this lane's row before its first tile
   if constexpr (MODE == FILL_TMA_G) lead = tmap.lead[lane & (tmap.g - 1)];
+  // FILL_TMA_G, this lane's row: row = lane_row0 + seg * R with R = 32 / g a
+  // multiple of 8 (g <= 4, tma_group_ok), so the swizzle key row & 7 is the
+  // same for every piece: one multiply-add per chunk instead of recomputing
+  // the row and its key (the generic taddr) for every 16-byte store
+  uint32_t g_lane_row0 = 0, g_rows_per_seg = 0, g_key = 0;
+  if constexpr (MODE == FILL_TMA_G) {
+    g_rows_per_seg = 32u >> tmap.gsh;
+    g_lane_row0 = (uint32_t)(lane & (tmap.g - 1)) * kSegs * g_rows_per_seg + (uint32_t)(lane >> tmap.gsh);
+    g_key = g_lane_row0 & 7u;
+  }
 
   extern __shared__ uint8_t smem_raw[];
   uint32_t tiles = 0;
@@ -317,7 +327,8 @@ __global__ void __launch_bounds__(kFillThreads)
         const int byte = e * ES;
         uint32_t addr;
         if constexpr (MODE == FILL_TMA_G)
-          addr = tile + taddr((int)(b * ES / 128) + (byte >> 7), lane, (byte & 127) >> 4);
+          addr = tile + ((g_lane_row0 + ((uint32_t)(b * ES / 128) + (uint32_t)(byte >> 7)) * g_rows_per_seg) << 7) +
+                 ((((uint32_t)(byte & 127) >> 4) ^ g_key) << 4);
         else
           addr = tile + ((b * ES / 128) << 12) + swz(byte >> 7, lane, (byte & 127) >> 4);
         if constexpr (ES == 8) {
