@@ -77,7 +77,12 @@ __host__ __device__ constexpr FillCfg fill_cfg_at(int i) {
   }
 }
 constexpr int kNumFillCfgs = 5;
-enum { FILL_KIND_NATIVE = 0, FILL_KIND_CONVERT = 1, FILL_KIND_CHECKSUM = 2, FILL_KIND_SHORT = 3 };
+enum { FILL_KIND_NATIVE = 0, FILL_KIND_CONVERT = 1, FILL_KIND_CHECKSUM = 2, FILL_KIND_SHORT = 3, FILL_KIND_GROUP = 4 };
+// row-group TMA (FILL_TMA_G, rows not 16-byte aligned): -DSLP_GROUP_CFG=i
+// gives that mode its own tile configuration (A/B); -1 = the tuned one
+#ifndef SLP_GROUP_CFG
+#define SLP_GROUP_CFG -1
+#endif
 }  // namespace dev
 }  // namespace slp
 #include "slp_fill_tuning.h"  // fill_tune(generator id, kind) -> configuration index (measured)
@@ -89,6 +94,7 @@ namespace dev {
 __host__ __device__ constexpr FillCfg fill_cfg(int id, int kind) {
   // short rows (T below one tuned tile): 256-byte pieces, two buffers
   if (kind == FILL_KIND_SHORT) return FillCfg{2, 2, 0, 32};
+  if (kind == FILL_KIND_GROUP) return fill_cfg_at(SLP_GROUP_CFG >= 0 ? SLP_GROUP_CFG : 0);
 #ifdef SLP_FILL_CFG
   return (void)id, (void)kind, fill_cfg_at(SLP_FILL_CFG);
 #else
@@ -203,7 +209,9 @@ __global__ void __launch_bounds__(kFillThreads)
   using bits = typename Cv::bits;
   constexpr int K = G::k;
   constexpr int ES = sizeof(bits);
-  using Shape = FillShape<G, SHORT ? (int)FILL_KIND_SHORT : fill_kind<OK, CSUM>()>;
+  using Shape = FillShape<G, SHORT ? (int)FILL_KIND_SHORT
+                                   : (MODE == FILL_TMA_G && SLP_GROUP_CFG >= 0 ? (int)FILL_KIND_GROUP
+                                                                               : fill_kind<OK, CSUM>())>;
   constexpr int kFillBufs = Shape::bufs, kSegs = Shape::segs, kTileBytes = Shape::tile_bytes;
   constexpr int CH = Shape::row_bytes / ES;                       // outputs per substream per tile
   constexpr int EPC = 16 / ES;                                    // elements per 16-byte chunk
@@ -989,7 +997,9 @@ int launch_fill_pos_cta(const FillParams &p, cudaStream_t st) {
 
 template <class G, int OK, int MODE, bool CSUM = false, bool SHORT = false, bool TAIL = false>
 int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) {
-  using Shape = FillShape<G, SHORT ? (int)FILL_KIND_SHORT : fill_kind<OK, CSUM>()>;
+  using Shape = FillShape<G, SHORT ? (int)FILL_KIND_SHORT
+                                   : (MODE == FILL_TMA_G && SLP_GROUP_CFG >= 0 ? (int)FILL_KIND_GROUP
+                                                                               : fill_kind<OK, CSUM>())>;
   using bits = typename Out<OK, typename G::word>::bits;
   constexpr int ES = sizeof(bits);
   FillParams p = p0;
@@ -1105,9 +1115,10 @@ int fill_impl(const FillParams &p, int out_kind, int layout, cudaStream_t st) {
   const bool short_rows = layout == SLP_STREAM_MAJOR && p.T < (uint64_t)segs * 128 / es;
   if (layout == SLP_STREAM_MAJOR) {
     const int ssegs = short_rows ? fill_cfg(0, FILL_KIND_SHORT).segs : segs;
+    const int gsegs = short_rows || SLP_GROUP_CFG < 0 ? ssegs : fill_cfg(0, FILL_KIND_GROUP).segs;
     mode = tma_ok(p.out, es, p.T, p.nstreams, p.ld_out, ssegs)
                ? FILL_TMA
-               : (tma_group_ok(p.out, es, p.T, p.nstreams, p.ld_out, ssegs) ? FILL_TMA_G : FILL_STAGED);
+               : (tma_group_ok(p.out, es, p.T, p.nstreams, p.ld_out, gsegs) ? FILL_TMA_G : FILL_STAGED);
     // stream-major segment rows (jsh > 0) are addressed through the 4-D store map only
     if (p.jsh && (mode != FILL_TMA || short_rows)) return SLP_ERR_UNSUPPORTED;
   }
