@@ -16,9 +16,11 @@ core, on BASELINE config 2's exact partition:
 * one step = every substream emits its next T = 1024 outputs into a (T, L)
   buffer (the reference's own ``chunks`` loop body, generators.py:476-480):
   ``buf[t] = spec.scrambler.apply_vec(st.word(S, i), st.word(S, j), w);
-  st.step(S)`` (scramblers.py:97-127, engines.py:318-361), with the states
-  kept resident in each worker and advanced in place — exactly the GPU arm's
-  step (bench.py: states resident in HBM, 1024 outputs per substream).
+  st.step(S)`` (scramblers.py:97-127, engines.py:318-361).  With
+  ``setup_each_step`` (bench.py's reference arm) the stock set-up above is
+  redone inside every step, from the seed, as the GPU arm's e2e leg does
+  (``Substreams.from_seed`` every step); without it the states stay resident
+  in each worker and advance in place (the GPU arm's kernel step).
 
 The first step from a fresh set-up is config 2 itself, so its wrapping sum
 and xor (reduced outside the timed steps) are checked against the golden
@@ -53,25 +55,31 @@ def import_reference():
     return slprng
 
 
-def _worker(conn, name, seed, s0, s1, T, chunk):
+def _worker(conn, name, seed, s0, s1, T, chunk, setup_each_step):
     R = import_reference()
     spec = R.get_spec(name)
     n = spec.kind.n
     J = 1 << (n // 2)
     sc = spec.scrambler
     w = spec.kind.w
+
+    def setup():
+        lanes = []
+        for c0 in range(s0, s1, chunk):
+            c1 = min(s1, c0 + chunk)
+            g = R.Generator.from_seed(spec, seed)
+            if c0:
+                g.jump(R.compute_jump_poly(spec, c0 * J))
+            ls = R.LanedStream(spec, generator=g, lanes=c1 - c0, lane_len=J)
+            lanes.append((ls.S, ls.stepper))
+        return lanes
+
     t0 = time.perf_counter()
-    lanes = []
-    for c0 in range(s0, s1, chunk):
-        c1 = min(s1, c0 + chunk)
-        g = R.Generator.from_seed(spec, seed)
-        if c0:
-            g.jump(R.compute_jump_poly(spec, c0 * J))
-        ls = R.LanedStream(spec, generator=g, lanes=c1 - c0, lane_len=J)
-        lanes.append((ls.S, ls.stepper))
+    lanes = setup()
     init_s = time.perf_counter() - t0
     buf = np.empty((T, min(chunk, max(1, s1 - s0))), dtype=np.uint64)
     conn.send(("ready", init_s))
+    first = True
     while True:
         cmd = conn.recv()
         if cmd == "stop":
@@ -79,6 +87,11 @@ def _worker(conn, name, seed, s0, s1, T, chunk):
         checksum = cmd == "step+checksum"
         acc_sum, acc_xor = 0, 0
         t0 = time.perf_counter()
+        setup_s = 0.0
+        if setup_each_step and not first:  # from the seed again: the stock lane set-up is part of the step
+            lanes = setup()
+            setup_s = time.perf_counter() - t0
+        first = False
         for S, st in lanes:
             L = S.shape[1]
             b = buf[:, :L]
@@ -90,7 +103,7 @@ def _worker(conn, name, seed, s0, s1, T, chunk):
             if checksum:  # only on the first (untimed, warm-up) step
                 acc_sum = (acc_sum + int(np.add.reduce(b, axis=None, dtype=np.uint64))) & ((1 << 64) - 1)
                 acc_xor ^= int(np.bitwise_xor.reduce(b, axis=None))
-        conn.send(("done", time.perf_counter() - t0, acc_sum, acc_xor))
+        conn.send(("done", time.perf_counter() - t0, acc_sum, acc_xor, setup_s))
 
 
 class ReferenceArm:
@@ -98,7 +111,7 @@ class ReferenceArm:
     the substreams with resident states (set up by the stock reference)."""
 
     def __init__(self, name="xoshiro256starstar", seed=42, n_streams=1 << 20, T=1024, procs=None,
-                 chunk=CHUNK):
+                 chunk=CHUNK, setup_each_step=False):
         import_reference()  # fail here, in the parent, if it is missing
         self.name, self.seed, self.n, self.T = name, seed, n_streams, T
         self.procs = max(1, min(procs or os.cpu_count() or 1, n_streams))
@@ -109,7 +122,7 @@ class ReferenceArm:
         for p in range(self.procs):
             s0, s1 = p * per, min(n_streams, (p + 1) * per)
             a, b = ctx.Pipe()
-            pr = ctx.Process(target=_worker, args=(b, name, seed, s0, s1, T, chunk), daemon=True)
+            pr = ctx.Process(target=_worker, args=(b, name, seed, s0, s1, T, chunk, setup_each_step), daemon=True)
             pr.start()
             self.conns.append(a)
             self.ps.append(pr)
@@ -120,13 +133,15 @@ class ReferenceArm:
 
     def step(self, checksum=False):
         """One step (T outputs per substream on every worker).  Returns
-        (outputs, wall seconds[, wrapping sum, xor])."""
+        (outputs, wall seconds[, wrapping sum, xor]); ``last_generate_s`` is
+        the slowest worker's step time without its set-up."""
         cmd = "step+checksum" if checksum else "step"
         t0 = time.perf_counter()
         for c in self.conns:
             c.send(cmd)
         res = [c.recv() for c in self.conns]
         wall = time.perf_counter() - t0
+        self.last_generate_s = max(r[1] - r[4] for r in res)
         self.steps_done += 1
         if checksum:
             s, x = 0, 0
