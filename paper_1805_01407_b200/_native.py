@@ -93,6 +93,7 @@ SIGNATURES = {
                                      ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, u64p, u64p, u64p, vp]),
     "slp_device_cache_bytes": (ctypes.c_size_t, [ctypes.c_int]),
+    "slp_set_fill_pace": (ctypes.c_int, [ctypes.c_int]),
     "slp_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "slp_last_error": (ctypes.c_char_p, []),
     "slp_build_info": (ctypes.c_char_p, []),

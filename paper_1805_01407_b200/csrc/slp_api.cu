@@ -111,6 +111,29 @@ int fill_grid_mult() {
   return v > 0 ? v : 1;
 }
 
+int fill_pace_burst() {
+  static int v = env_int("SLP_FILL_PACE_BURST", 1);
+  return v > 0 ? v : 1;
+}
+
+int fill_pace_mode() {
+  static int v = env_int("SLP_FILL_PACE_MODE", 0);
+  return v;
+}
+
+// store pacing of the TMA fill modes (pace_store in slp_gen.cuh): the target
+// aggregate store rate in GB/s, SLP_FILL_PACE_GBPS or slp_set_fill_pace; 0 = off
+static std::atomic<int> g_pace_gbps{-1};
+int fill_pace_gbps() {
+  int v = g_pace_gbps.load(std::memory_order_relaxed);
+  if (v < 0) {
+    v = env_int("SLP_FILL_PACE_GBPS", kDefaultPaceGbps);
+    if (v < 0) v = 0;
+    g_pace_gbps.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 int cuda_fail(const char *what) {
   cudaError_t e = cudaGetLastError();
   set_last_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -1145,6 +1168,12 @@ int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, ui
   p.overflow_ctas = reinterpret_cast<unsigned long long *>(overflow_ctas);
   if (nthreads == 0) return SLP_OK;
   return ops->hwd(p, transitional, split, static_cast<cudaStream_t>(stream));
+}
+
+int slp_set_fill_pace(int gbps) {
+  const int prev = fill_pace_gbps();
+  if (gbps >= 0) g_pace_gbps.store(gbps, std::memory_order_relaxed);
+  return prev;
 }
 
 size_t slp_device_cache_bytes(int device) {

@@ -73,6 +73,8 @@ __host__ __device__ constexpr FillCfg fill_cfg_at(int i) {
     case 3: return FillCfg{4, 2, 0, 32};  // 512 B rows, two buffers
     case 4: return FillCfg{4, 2, 0, 64};
     case 5: return FillCfg{4, 1, 16, 32};  // 512 B rows, one buffer (A/B builds only)
+    case 6: return FillCfg{6, 1, 16, 32};  // 768 B rows, one buffer (A/B builds with 9 warps)
+    case 7: return FillCfg{5, 1, 8, 16};   // 640 B rows, one buffer (A/B builds with 11 warps)
     default: return FillCfg{8, 1, 16, 32};  // 0: 1 KiB rows, one buffer
   }
 }
@@ -88,6 +90,11 @@ enum { FILL_KIND_NATIVE = 0, FILL_KIND_CONVERT = 1, FILL_KIND_CHECKSUM = 2, FILL
 #include "slp_fill_tuning.h"  // fill_tune(generator id, kind) -> configuration index (measured)
 namespace slp {
 namespace dev {
+
+#ifndef SLP_STS_BATCH
+#define SLP_STS_BATCH 1
+#endif
+constexpr int kStsBatch = SLP_STS_BATCH;
 
 // -DSLP_FILL_CFG=i forces configuration i for every kernel (tuning builds,
 // profiles/tune_fill.py)
@@ -216,6 +223,8 @@ __global__ void __launch_bounds__(kFillThreads)
   constexpr int CH = Shape::row_bytes / ES;                       // outputs per substream per tile
   constexpr int EPC = 16 / ES;                                    // elements per 16-byte chunk
   constexpr int U = Shape::unroll < CH ? Shape::unroll : CH;       // outputs per sub-block
+  // chunks generated per batch of shared stores (SLP_STS_BATCH; clamped to the sub-block)
+  constexpr int NB = (U / EPC) % kStsBatch == 0 ? kStsBatch : 1;
   static_assert(CH % U == 0 && U % EPC == 0 && (U * ES) % 128 == 0, "sub-blocks must be whole 128-byte segments");
   static_assert(!G::ring || U % K == 0, "sub-blocks must cover whole ring periods");
   // 16-byte chunks produced before the buffer wait (at most one sub-block)
@@ -258,6 +267,13 @@ __global__ void __launch_bounds__(kFillThreads)
   if constexpr (MODE == FILL_TMA_G) ntiles = (p.T - tmap.lead_max) / CH;  // tiles every row has after its lead
   const uint64_t rem = p.T - ntiles * CH;
   uint32_t issued = 0;  // tiles produced by this warp
+  uint64_t pace_next = 0;  // store pacing: earliest issue time (global ns) of this warp's next tile store
+#ifdef SLP_FILL_DBG_NOSTS
+  uint64_t dbg_sink = 0;
+#endif
+  __shared__ unsigned long long cta_pace_next;  // store pacing, CTA-shared schedule
+  if (threadIdx.x == 0) cta_pace_next = 0;
+  __syncthreads();
   uint64_t cs_lo = 0, cs_hi = 0, cs_x = 0, cs_low = 0;  // CSUM accumulators (zero states emit zeros)
 
   // the next unit's start states are loaded while this unit is generated
@@ -320,6 +336,13 @@ __global__ void __launch_bounds__(kFillThreads)
       // one 16-byte chunk (outputs b+e .. b+e+EPC-1 of this lane's row) into the
       // tile; b (runtime) is a sub-block start, e (compile time) the offset in it
       auto put = [&](uint32_t b, int e, const bits(&v)[EPC]) {
+#ifdef SLP_FILL_DBG_NOSTS  // measurement builds only: generation without the shared stores
+        if constexpr (MODE == FILL_TMA) {
+#pragma unroll
+          for (int i = 0; i < EPC; ++i) dbg_sink ^= (uint64_t)v[i];
+          return;
+        }
+#endif
         if constexpr (MODE == FILL_POS_TMA) {  // tile [position][lane]
           const uint32_t row = tile + (b * 32 + lane) * ES;
 #pragma unroll
@@ -430,11 +453,17 @@ __global__ void __launch_bounds__(kFillThreads)
       // generator is ~60 KB of SASS, twice the 32 KB L1.5 I-cache)
 #pragma unroll 1
       for (uint32_t b = U; b < sub_end; b += U) {
+        // NB chunks are generated before their NB shared stores issue: each
+        // STS.128 then reads its own registers, instead of every store
+        // sourcing the same quad that the next output overwrites (a
+        // read-barrier wait per store)
 #pragma unroll
-        for (int e = 0; e < U; e += EPC) {
-          bits v[EPC];
-          gen(e, v);
-          emit(b, e, v);
+        for (int e = 0; e < U; e += EPC * NB) {
+          bits v[NB][EPC];
+#pragma unroll
+          for (int j = 0; j < NB; ++j) gen(e + j * EPC, v[j]);
+#pragma unroll
+          for (int j = 0; j < NB; ++j) emit(b, e + j * EPC, v[j]);
         }
       }
       if constexpr (CSUM) {
@@ -452,15 +481,28 @@ __global__ void __launch_bounds__(kFillThreads)
       }
       if constexpr (MODE == FILL_TMA) {
         fence_proxy_async_smem();
+        if (p.pace_ns) {
+          if (p.pace_cta)
+            pace_store_cta(&cta_pace_next, p.pace_ns / kFillWarps);
+          else
+            pace_store(pace_next, p.pace_ns, p.pace_burst);
+        }
         __syncwarp();
         if (elect_one()) {
-          tma_store_4d(&tmap, tile, 0, (int)(row0 & ((1ull << p.jsh) - 1)), (int)(row0 >> p.jsh),
-                       (int)(pos0 * ES / 128));
+          if (!p.no_store)
+            tma_store_4d(&tmap, tile, 0, (int)(row0 & ((1ull << p.jsh) - 1)), (int)(row0 >> p.jsh),
+                         (int)(pos0 * ES / 128));
           bulk_commit();
         }
         ++issued;
       } else if constexpr (MODE == FILL_POS_TMA) {
         fence_proxy_async_smem();
+        if (p.pace_ns) {
+          if (p.pace_cta)
+            pace_store_cta(&cta_pace_next, p.pace_ns / kFillWarps);
+          else
+            pace_store(pace_next, p.pace_ns, p.pace_burst);
+        }
         __syncwarp();
         if (elect_one()) {
           uint64_t roff, col0;
@@ -471,6 +513,12 @@ __global__ void __launch_bounds__(kFillThreads)
         ++issued;
       } else if constexpr (MODE == FILL_TMA_G) {
         fence_proxy_async_smem();
+        if (p.pace_ns) {
+          if (p.pace_cta)
+            pace_store_cta(&cta_pace_next, p.pace_ns / kFillWarps);
+          else
+            pace_store(pace_next, p.pace_ns, p.pace_burst);
+        }
         __syncwarp();
         if (elect_one()) {
           store_groups(tile, row0, pos0 * ES / 128, nullptr);
@@ -721,6 +769,9 @@ __global__ void __launch_bounds__(kFillThreads)
     if (elect_one()) bulk_wait_all<0>();
   }
   if constexpr (CSUM) reduce_checksum_block<kFillWarps>(cs_lo, cs_hi, cs_x, cs_low, 0.0, p.partials);
+#ifdef SLP_FILL_DBG_NOSTS
+  if (dbg_sink == 0x0123456789abcdefull) out[0] = (bits)dbg_sink;
+#endif
 }
 
 
@@ -1043,6 +1094,23 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
     if ((uint64_t)grid * sizeof(slp_checksum) > p.workspace_bytes) return SLP_ERR_BUFFER;
   }
   if (grid_out) *grid_out = (int)grid;
+  p.pace_ns = 0;
+  if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA || MODE == FILL_TMA_G) {
+    // the whole fill should take bytes / fill_pace_gbps (bytes per ns); the
+    // busiest warp stores ceil(units / warps) x tiles-per-unit tiles in that time
+    const int gbps = fill_pace_gbps();
+    if (gbps > 0) {
+      const uint64_t warps = (uint64_t)grid * kFillWarps;
+      const uint64_t tiles_per_unit = (p.T + Shape::row_bytes / ES - 1) / (Shape::row_bytes / ES);
+      const uint64_t tiles_max = (p.nunits + warps - 1) / warps * tiles_per_unit;
+      const double ns = (double)p.nunits * tiles_per_unit * Shape::tile_bytes / gbps;
+      p.pace_ns = tiles_max ? (uint32_t)(ns / (double)tiles_max) : 0u;
+    }
+    p.pace_cta = fill_pace_mode() == 1;
+    p.pace_burst = (uint32_t)fill_pace_burst();
+    static const bool no_store = std::getenv("SLP_FILL_NO_STORE") != nullptr;
+    p.no_store = no_store;
+  }
   kern<<<grid, kFillThreads, smem, st>>>(p, tmap);
   return check_launch("k_fill");
 }

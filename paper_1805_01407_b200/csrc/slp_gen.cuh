@@ -575,6 +575,40 @@ __device__ __forceinline__ bool elect_one() {
       : "=r"(pred));
   return pred != 0;
 }
+// store pacing (k_fill): HBM absorbs a stream of row-piece stores at ~6.7 TB/s
+// when they are offered at about that rate, but only ~6.1 TB/s when the
+// offered rate exceeds it (profiles/wpattern_r3.cu, round2_wpattern_r3*.jsonl);
+// a warp therefore issues its tile stores no closer than pace_ns apart on the
+// global timer.  A warp that fell behind catches up by at most `burst` periods.
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void pace_store(uint64_t &next, uint32_t pace_ns, uint32_t burst) {
+  uint64_t now = global_ns();
+  while (now < next) now = global_ns();
+  now = __shfl_sync(0xffffffffu, now, 0);
+  // a warp more than `burst` periods behind its schedule restarts it at now
+  next = (now > next + (uint64_t)burst * pace_ns ? now : next) + pace_ns;
+}
+// CTA-wide variant: the CTA's warps share one schedule of slots spaced
+// pace_ns / warps apart, so a ready warp takes the next free slot (a warp's
+// jitter is absorbed by the others); a schedule that fell more than two slots
+// behind restarts at the current time
+__device__ __forceinline__ void pace_store_cta(unsigned long long *next, uint32_t slot_ns) {
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long now = global_ns();
+    unsigned long long slot = atomicAdd(next, (unsigned long long)slot_ns);
+    if (slot + 2ull * slot_ns < now) {
+      atomicMax(next, now + slot_ns);
+      slot = now;
+    }
+    while (global_ns() < slot) {
+    }
+  }
+  __syncwarp();
+}
 // 128-bit accumulate of a 64-bit value
 __device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t x) {
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(lo), "+l"(hi) : "l"(x));

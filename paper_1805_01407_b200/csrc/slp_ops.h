@@ -39,6 +39,12 @@ struct FillParams {
   // [j * T, (j + 1) * T).  jsh = 0 and pm_n = 0: no split.
   uint32_t jsh;
   uint64_t pm_n;
+  // store pacing (TMA modes of k_fill): minimum ns between one warp's tile
+  // stores, set by the launcher from the target rate (0 = unpaced)
+  uint32_t pace_ns;
+  uint32_t pace_cta;  // 1: the CTA's warps share one slot schedule (pace_store_cta)
+  uint32_t pace_burst;  // periods a late warp may catch up (pace_store)
+  uint32_t no_store;  // measurement only (SLP_FILL_NO_STORE=1): generate tiles, skip the TMA stores
 };
 
 struct FusedParams {
@@ -96,6 +102,11 @@ struct TableJumpParams {
 #define SLP_FILL_WARPS 7
 #endif
 constexpr int kFillWarps = SLP_FILL_WARPS;
+// default store-pacing target of the TMA fill modes in GB/s (0 = unpaced)
+#ifndef SLP_DEFAULT_PACE_GBPS
+#define SLP_DEFAULT_PACE_GBPS 0
+#endif
+constexpr int kDefaultPaceGbps = SLP_DEFAULT_PACE_GBPS;
 
 // up to 16 batches (long-jump blocks) x 16 words, passed by value
 constexpr int kMaxBaseBatches = 16;
@@ -142,6 +153,9 @@ const GenOps *gen_ops(int id);
 int current_device();
 int sm_count(int dev);
 int fill_grid_mult();
+int fill_pace_gbps();  // store pacing target in GB/s (0 = off), slp_set_fill_pace
+int fill_pace_burst();  // SLP_FILL_PACE_BURST
+int fill_pace_mode();  // 0 per-warp schedule, 1 CTA-shared schedule (SLP_FILL_PACE_MODE)
 int cuda_fail(const char *what);
 int check_launch(const char *what);
 bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);

@@ -162,6 +162,15 @@ def fill(spec: GeneratorSpec, states: torch.Tensor, T: int, *, out: torch.Tensor
     return out
 
 
+def set_fill_pace(gbps: int | None) -> int:
+    """Store pacing of the fill kernels (C ABI ``slp_set_fill_pace``): their
+    tile stores are offered at no more than ``gbps`` GB/s in aggregate, which
+    HBM absorbs faster than an unpaced stream.  0 turns pacing
+    off, None only queries.  Returns the previous target.  Results never
+    depend on it."""
+    return int(_native.lib().slp_set_fill_pace(-1 if gbps is None else int(gbps)))
+
+
 def _split_factor(spec: GeneratorSpec, n: int, T: int, layout: str, ld_out: int, es: int | None = None) -> int:
     """Segments per substream the C ABI uses internally for few, long
     substreams (slp_split_factor): contiguous and padded stream-major rows

@@ -99,3 +99,16 @@ def test_split_factor_is_host_only_and_follows_the_wave_rule():
     big = L.slp_generator_id(b"xoroshiro1024starstar")
     assert (1 << 20) // L.slp_split_factor(big, 1, 1 << 20) >= 2 * 1024  # >= 2 outputs per state bit
     assert (1 << 28) // L.slp_split_factor(big, 1, 1 << 28) >= 8 * 1024  # long rows: >= 8 per state bit
+
+
+def test_fill_pace_knob_is_host_only():
+    """slp_set_fill_pace: query with a negative value, set, restore (no device call)."""
+    from paper_1805_01407_b200 import device as D
+
+    L = _native.lib()
+    cur = L.slp_set_fill_pace(-1)
+    assert cur >= 0
+    assert L.slp_set_fill_pace(1234) == cur
+    assert D.set_fill_pace(None) == 1234
+    assert D.set_fill_pace(cur) == 1234
+    assert L.slp_set_fill_pace(-1) == cur
