@@ -293,10 +293,11 @@ def run_ours(args):
                 "write_only_ceiling_gbs": round(write_only_gbs, 1),
                 "frac_of_write_only_ceiling": round(achieved / write_only_gbs, 4),
                 "write_only_note": "forward-sweep fill_ of the same 8 GiB tensor, measured live on this GPU",
-                "frac_of_write_pattern_ceiling": round(achieved / 6152.0, 4),
-                "write_pattern_ceiling_note": "6152 GB/s = TMA-only store of the same stream-major pattern and "
-                                              "geometry (1 KiB row pieces, 7 warps x 1 buffer, no generation), "
-                                              "profiles/round1_write_patterns.md"}
+                "frac_of_write_pattern_ceiling": round(achieved / 6708.0, 4),
+                "write_pattern_ceiling_note": "6708 GB/s = best TMA-only store of the same stream-major pattern and "
+                                              "geometry (1 KiB row pieces, 7 warps x 1 buffer, no generation) under "
+                                              "store pacing; 6106 unpaced (profiles/round2_pacing.md)",
+                "store_pacing_gbps": D.set_fill_pace(None)}
 
     # e2e: public API from the seed to HOST memory, every step: substream init
     # (H2D: the base state, k words) + fill + D2H of all outputs (pinned), overlapped

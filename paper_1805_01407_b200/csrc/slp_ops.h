@@ -104,7 +104,7 @@ struct TableJumpParams {
 constexpr int kFillWarps = SLP_FILL_WARPS;
 // default store-pacing target of the TMA fill modes in GB/s (0 = unpaced)
 #ifndef SLP_DEFAULT_PACE_GBPS
-#define SLP_DEFAULT_PACE_GBPS 0
+#define SLP_DEFAULT_PACE_GBPS 6500
 #endif
 constexpr int kDefaultPaceGbps = SLP_DEFAULT_PACE_GBPS;
 
