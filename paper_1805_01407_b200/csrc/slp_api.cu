@@ -112,13 +112,8 @@ int fill_grid_mult() {
 }
 
 int fill_pace_burst() {
-  static int v = env_int("SLP_FILL_PACE_BURST", 1);
+  static int v = env_int("SLP_FILL_PACE_BURST", 4);
   return v > 0 ? v : 1;
-}
-
-int fill_pace_mode() {
-  static int v = env_int("SLP_FILL_PACE_MODE", 0);
-  return v;
 }
 
 // store pacing of the TMA fill modes (pace_store in slp_gen.cuh): the target

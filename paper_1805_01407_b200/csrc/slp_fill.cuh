@@ -91,11 +91,6 @@ enum { FILL_KIND_NATIVE = 0, FILL_KIND_CONVERT = 1, FILL_KIND_CHECKSUM = 2, FILL
 namespace slp {
 namespace dev {
 
-#ifndef SLP_STS_BATCH
-#define SLP_STS_BATCH 1
-#endif
-constexpr int kStsBatch = SLP_STS_BATCH;
-
 // -DSLP_FILL_CFG=i forces configuration i for every kernel (tuning builds,
 // profiles/tune_fill.py)
 __host__ __device__ constexpr FillCfg fill_cfg(int id, int kind) {
@@ -223,8 +218,6 @@ __global__ void __launch_bounds__(kFillThreads)
   constexpr int CH = Shape::row_bytes / ES;                       // outputs per substream per tile
   constexpr int EPC = 16 / ES;                                    // elements per 16-byte chunk
   constexpr int U = Shape::unroll < CH ? Shape::unroll : CH;       // outputs per sub-block
-  // chunks generated per batch of shared stores (SLP_STS_BATCH; clamped to the sub-block)
-  constexpr int NB = (U / EPC) % kStsBatch == 0 ? kStsBatch : 1;
   static_assert(CH % U == 0 && U % EPC == 0 && (U * ES) % 128 == 0, "sub-blocks must be whole 128-byte segments");
   static_assert(!G::ring || U % K == 0, "sub-blocks must cover whole ring periods");
   // 16-byte chunks produced before the buffer wait (at most one sub-block)
@@ -271,9 +264,6 @@ __global__ void __launch_bounds__(kFillThreads)
 #ifdef SLP_FILL_DBG_NOSTS
   uint64_t dbg_sink = 0;
 #endif
-  __shared__ unsigned long long cta_pace_next;  // store pacing, CTA-shared schedule
-  if (threadIdx.x == 0) cta_pace_next = 0;
-  __syncthreads();
   uint64_t cs_lo = 0, cs_hi = 0, cs_x = 0, cs_low = 0;  // CSUM accumulators (zero states emit zeros)
 
   // the next unit's start states are loaded while this unit is generated
@@ -453,17 +443,11 @@ __global__ void __launch_bounds__(kFillThreads)
       // generator is ~60 KB of SASS, twice the 32 KB L1.5 I-cache)
 #pragma unroll 1
       for (uint32_t b = U; b < sub_end; b += U) {
-        // NB chunks are generated before their NB shared stores issue: each
-        // STS.128 then reads its own registers, instead of every store
-        // sourcing the same quad that the next output overwrites (a
-        // read-barrier wait per store)
 #pragma unroll
-        for (int e = 0; e < U; e += EPC * NB) {
-          bits v[NB][EPC];
-#pragma unroll
-          for (int j = 0; j < NB; ++j) gen(e + j * EPC, v[j]);
-#pragma unroll
-          for (int j = 0; j < NB; ++j) emit(b, e + j * EPC, v[j]);
+        for (int e = 0; e < U; e += EPC) {
+          bits v[EPC];
+          gen(e, v);
+          emit(b, e, v);
         }
       }
       if constexpr (CSUM) {
@@ -481,12 +465,7 @@ __global__ void __launch_bounds__(kFillThreads)
       }
       if constexpr (MODE == FILL_TMA) {
         fence_proxy_async_smem();
-        if (p.pace_ns) {
-          if (p.pace_cta)
-            pace_store_cta(&cta_pace_next, p.pace_ns / kFillWarps);
-          else
-            pace_store(pace_next, p.pace_ns, p.pace_burst);
-        }
+        if (p.pace_ns) pace_store(pace_next, p.pace_ns, p.pace_burst);
         __syncwarp();
         if (elect_one()) {
           if (!p.no_store)
@@ -497,12 +476,7 @@ __global__ void __launch_bounds__(kFillThreads)
         ++issued;
       } else if constexpr (MODE == FILL_POS_TMA) {
         fence_proxy_async_smem();
-        if (p.pace_ns) {
-          if (p.pace_cta)
-            pace_store_cta(&cta_pace_next, p.pace_ns / kFillWarps);
-          else
-            pace_store(pace_next, p.pace_ns, p.pace_burst);
-        }
+        if (p.pace_ns) pace_store(pace_next, p.pace_ns, p.pace_burst);
         __syncwarp();
         if (elect_one()) {
           uint64_t roff, col0;
@@ -513,12 +487,7 @@ __global__ void __launch_bounds__(kFillThreads)
         ++issued;
       } else if constexpr (MODE == FILL_TMA_G) {
         fence_proxy_async_smem();
-        if (p.pace_ns) {
-          if (p.pace_cta)
-            pace_store_cta(&cta_pace_next, p.pace_ns / kFillWarps);
-          else
-            pace_store(pace_next, p.pace_ns, p.pace_burst);
-        }
+        if (p.pace_ns) pace_store(pace_next, p.pace_ns, p.pace_burst);
         __syncwarp();
         if (elect_one()) {
           store_groups(tile, row0, pos0 * ES / 128, nullptr);
@@ -784,6 +753,23 @@ __global__ void __launch_bounds__(kFillThreads)
 // one 2-D TMA store of 64 x 64; two 16 KB buffers per warp.
 constexpr int kPm2Pos = 64;
 constexpr int kPm2TileBytes = kPm2Pos * 64 * 4;
+
+// store pacing period (pace_store): `units` units of work spread over `agents`
+// (warps or CTAs) that each store `tiles_per_unit` tiles of `tile_bytes` per
+// unit; the whole fill should take bytes / fill_pace_gbps (bytes per ns), and
+// the busiest agent stores ceil(units / agents) x tiles_per_unit tiles in that
+// time.  0 = unpaced.
+// Position-major tiles (8 MiB-apart rows of 256 B) congest earlier: they are
+// paced at 95% of the target (measured best at 6200 where stream-major rows
+// are best at 6500, profiles/round2_pace_modes*.jsonl).
+inline uint32_t pace_period_ns(uint64_t units, uint64_t agents, uint64_t tiles_per_unit, uint64_t tile_bytes,
+                               bool position_major = false) {
+  const int gbps = position_major ? fill_pace_gbps() * 95 / 100 : fill_pace_gbps();
+  if (gbps <= 0 || !units || !agents || !tiles_per_unit) return 0;
+  const uint64_t tiles_max = (units + agents - 1) / agents * tiles_per_unit;
+  const double ns = (double)units * tiles_per_unit * tile_bytes / gbps;
+  return (uint32_t)(ns / (double)tiles_max);
+}
 constexpr int kPm2Smem = kFillWarps * 2 * kPm2TileBytes + 1024;
 
 template <class G, int OK>
@@ -805,6 +791,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pm2(FillParams p, const _
   const uint64_t ntiles = p.T / kPm2Pos, rem = p.T - ntiles * kPm2Pos;
   const uint64_t nunits = (p.nstreams + 63) / 64;
   uint32_t issued = 0;
+  uint64_t pace_next = 0;  // store pacing (pace_store)
   for (uint64_t u = (uint64_t)blockIdx.x * kFillWarps + warp; u < nunits; u += (uint64_t)gridDim.x * kFillWarps) {
     const uint64_t row0 = u * 64;
     const uint64_t stA = row0 + lane, stB = row0 + 32 + lane;
@@ -831,6 +818,7 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_pm2(FillParams p, const _
         asm volatile("st.shared.b32 [%0], %1;" ::"r"(row + 128), "r"((uint32_t)xb) : "memory");
       }
       fence_proxy_async_smem();
+      if (p.pace_ns) pace_store(pace_next, p.pace_ns, p.pace_burst);
       __syncwarp();
       if (elect_one()) {
         uint64_t roff, col0;
@@ -882,7 +870,10 @@ int launch_fill_pm2(const FillParams &p, cudaStream_t st) {
   const uint64_t want = (nunits + kFillWarps - 1) / kFillWarps;
   const uint64_t cap = (uint64_t)sm_count(dev) * fill_grid_mult();
   const unsigned grid = (unsigned)(want < cap ? want : cap);
-  kern<<<grid, kFillThreads, kPm2Smem, st>>>(p, tmap);
+  FillParams q = p;
+  q.pace_ns = pace_period_ns(nunits, (uint64_t)grid * kFillWarps, p.T / kPm2Pos, kPm2TileBytes, true);
+  q.pace_burst = (uint32_t)fill_pace_burst();
+  kern<<<grid, kFillThreads, kPm2Smem, st>>>(q, tmap);
   return check_launch("k_fill_pm2");
 }
 
@@ -1042,7 +1033,10 @@ int launch_fill_pos_cta(const FillParams &p, cudaStream_t st) {
   if (nblk == 0 || p.T == 0) return SLP_OK;
   const uint64_t cap = (uint64_t)sm_count(dev) * per_sm[dev] * fill_grid_mult();
   const unsigned grid = (unsigned)(nblk < cap ? nblk : cap);
-  kern<<<grid, kFillThreads, PC::SMEM, st>>>(p);
+  // (not paced: measured 8-18% slower paced; the kernel is generation-bound)
+  FillParams q = p;
+  q.pace_ns = 0;
+  kern<<<grid, kFillThreads, PC::SMEM, st>>>(q);
   return check_launch("k_fill_pos_cta");
 }
 
@@ -1095,18 +1089,11 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
   }
   if (grid_out) *grid_out = (int)grid;
   p.pace_ns = 0;
-  if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA || MODE == FILL_TMA_G) {
-    // the whole fill should take bytes / fill_pace_gbps (bytes per ns); the
-    // busiest warp stores ceil(units / warps) x tiles-per-unit tiles in that time
-    const int gbps = fill_pace_gbps();
-    if (gbps > 0) {
-      const uint64_t warps = (uint64_t)grid * kFillWarps;
-      const uint64_t tiles_per_unit = (p.T + Shape::row_bytes / ES - 1) / (Shape::row_bytes / ES);
-      const uint64_t tiles_max = (p.nunits + warps - 1) / warps * tiles_per_unit;
-      const double ns = (double)p.nunits * tiles_per_unit * Shape::tile_bytes / gbps;
-      p.pace_ns = tiles_max ? (uint32_t)(ns / (double)tiles_max) : 0u;
-    }
-    p.pace_cta = fill_pace_mode() == 1;
+  // (row-group rows of 4-byte outputs measured 3-6% slower paced: not paced)
+  if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA || (MODE == FILL_TMA_G && ES == 8)) {
+    const uint64_t tiles_per_unit = (p.T + Shape::row_bytes / ES - 1) / (Shape::row_bytes / ES);
+    p.pace_ns = pace_period_ns(p.nunits, (uint64_t)grid * kFillWarps, tiles_per_unit, Shape::tile_bytes,
+                               MODE == FILL_POS_TMA);
     p.pace_burst = (uint32_t)fill_pace_burst();
     static const bool no_store = std::getenv("SLP_FILL_NO_STORE") != nullptr;
     p.no_store = no_store;

@@ -592,23 +592,6 @@ __device__ __forceinline__ void pace_store(uint64_t &next, uint32_t pace_ns, uin
   // a warp more than `burst` periods behind its schedule restarts it at now
   next = (now > next + (uint64_t)burst * pace_ns ? now : next) + pace_ns;
 }
-// CTA-wide variant: the CTA's warps share one schedule of slots spaced
-// pace_ns / warps apart, so a ready warp takes the next free slot (a warp's
-// jitter is absorbed by the others); a schedule that fell more than two slots
-// behind restarts at the current time
-__device__ __forceinline__ void pace_store_cta(unsigned long long *next, uint32_t slot_ns) {
-  if ((threadIdx.x & 31) == 0) {
-    const unsigned long long now = global_ns();
-    unsigned long long slot = atomicAdd(next, (unsigned long long)slot_ns);
-    if (slot + 2ull * slot_ns < now) {
-      atomicMax(next, now + slot_ns);
-      slot = now;
-    }
-    while (global_ns() < slot) {
-    }
-  }
-  __syncwarp();
-}
 // 128-bit accumulate of a 64-bit value
 __device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t x) {
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(lo), "+l"(hi) : "l"(x));

@@ -42,7 +42,6 @@ struct FillParams {
   // store pacing (TMA modes of k_fill): minimum ns between one warp's tile
   // stores, set by the launcher from the target rate (0 = unpaced)
   uint32_t pace_ns;
-  uint32_t pace_cta;  // 1: the CTA's warps share one slot schedule (pace_store_cta)
   uint32_t pace_burst;  // periods a late warp may catch up (pace_store)
   uint32_t no_store;  // measurement only (SLP_FILL_NO_STORE=1): generate tiles, skip the TMA stores
 };
@@ -155,7 +154,6 @@ int sm_count(int dev);
 int fill_grid_mult();
 int fill_pace_gbps();  // store pacing target in GB/s (0 = off), slp_set_fill_pace
 int fill_pace_burst();  // SLP_FILL_PACE_BURST
-int fill_pace_mode();  // 0 per-warp schedule, 1 CTA-shared schedule (SLP_FILL_PACE_MODE)
 int cuda_fail(const char *what);
 int check_launch(const char *what);
 bool tma_ok(const void *out, int es, uint64_t T, uint64_t nstreams, uint64_t ld_out, int segs);

@@ -30,7 +30,7 @@ def main():
     h = pynvml.nvmlDeviceGetHandleByIndex(0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for case in cases:
-        gen, n, T, kind, layout = CASES[case]
+        gen, n, T, kind, layout = CASES[case][:5]
         spec = P.get_spec(gen)
         sub = D.Substreams.from_seed(spec, 42, n)
         out = sub.fill(T, kind=kind, layout=layout)

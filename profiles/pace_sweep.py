@@ -29,6 +29,15 @@ CASES = {
     "x1024": ("xoroshiro1024plusplus", 1 << 20, 1024, "native", "stream"),
     "pm": ("xoshiro256starstar", 1 << 20, 1024, "native", "position"),
     "t2048": ("xoshiro256starstar", 1 << 19, 2048, "native", "stream"),
+    "oddT": ("xoshiro256starstar", 1 << 20, 1023, "native", "stream"),
+    "oddT32": ("xoshiro128starstar", 1 << 21, 1023, "native", "stream"),
+    "pmf64": ("xoroshiro128plus", 1 << 20, 1024, "f64", "position"),
+    "pm1024": ("xoroshiro1024plusplus", 1 << 20, 1024, "native", "position"),
+    "pm32": ("xoshiro128starstar", 1 << 21, 1024, "native", "position"),
+    "pmf32": ("xoshiro128starstar", 1 << 21, 1024, "f32", "position"),
+    # odd pitch (one element of padding per row): CTA-staged position-major path
+    "pmodd": ("xoshiro256starstar", 1 << 20, 1024, "native", "position", 1),
+    "pmodd32": ("xoshiro128starstar", 1 << 21, 1024, "native", "position", 1),
 }
 
 
@@ -42,10 +51,14 @@ def main():
     targets = [int(x) for x in a.targets.split(",")]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for case in a.cases.split(","):
-        gen, n, T, kind, layout = CASES[case]
+        gen, n, T, kind, layout = CASES[case][:5]
+        pad = CASES[case][5] if len(CASES[case]) > 5 else 0
         spec = P.get_spec(gen)
         sub = D.Substreams.from_seed(spec, 42, n)
         out = sub.fill(T, kind=kind, layout=layout)
+        if pad:
+            rows, cols = out.shape
+            out = torch.empty((rows, cols + pad), dtype=out.dtype, device=out.device)[:, :cols]
         nbytes = out.numel() * out.element_size()
 
         def timed(target):
