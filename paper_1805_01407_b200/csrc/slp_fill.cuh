@@ -759,12 +759,15 @@ constexpr int kPm2TileBytes = kPm2Pos * 64 * 4;
 // unit; the whole fill should take bytes / fill_pace_gbps (bytes per ns), and
 // the busiest agent stores ceil(units / agents) x tiles_per_unit tiles in that
 // time.  0 = unpaced.
-// Position-major tiles (8 MiB-apart rows of 256 B) congest earlier: they are
-// paced at 95% of the target (measured best at 6200 where stream-major rows
-// are best at 6500, profiles/round2_pace_modes*.jsonl).
+// Position-major tiles (8 MiB-apart rows of 256 B) and the 1024-bit engine
+// (16-word states read and written around every unit) congest earlier: each
+// is paced at 95% of the target (measured best at ~6200 where stream-major
+// rows of the small engines are best at 6500, profiles/round2_pace_*.jsonl).
 inline uint32_t pace_period_ns(uint64_t units, uint64_t agents, uint64_t tiles_per_unit, uint64_t tile_bytes,
-                               bool position_major = false) {
-  const int gbps = position_major ? fill_pace_gbps() * 95 / 100 : fill_pace_gbps();
+                               bool position_major = false, bool wide_state = false) {
+  int gbps = fill_pace_gbps();
+  if (position_major) gbps = gbps * 95 / 100;
+  if (wide_state) gbps = gbps * 95 / 100;
   if (gbps <= 0 || !units || !agents || !tiles_per_unit) return 0;
   const uint64_t tiles_max = (units + agents - 1) / agents * tiles_per_unit;
   const double ns = (double)units * tiles_per_unit * tile_bytes / gbps;
@@ -1089,11 +1092,12 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
   }
   if (grid_out) *grid_out = (int)grid;
   p.pace_ns = 0;
-  // (row-group rows of 4-byte outputs measured 3-6% slower paced: not paced)
-  if constexpr (MODE == FILL_TMA || MODE == FILL_POS_TMA || (MODE == FILL_TMA_G && ES == 8)) {
+  // (not paced, measured slower paced: row-group rows of 4-byte outputs (3-6%)
+  // and store + checksum, which is generation-bound (up to 8%))
+  if constexpr (!CSUM && (MODE == FILL_TMA || MODE == FILL_POS_TMA || (MODE == FILL_TMA_G && ES == 8))) {
     const uint64_t tiles_per_unit = (p.T + Shape::row_bytes / ES - 1) / (Shape::row_bytes / ES);
     p.pace_ns = pace_period_ns(p.nunits, (uint64_t)grid * kFillWarps, tiles_per_unit, Shape::tile_bytes,
-                               MODE == FILL_POS_TMA);
+                               MODE == FILL_POS_TMA, G::k * G::w >= 1024);
     p.pace_burst = (uint32_t)fill_pace_burst();
     static const bool no_store = std::getenv("SLP_FILL_NO_STORE") != nullptr;
     p.no_store = no_store;

@@ -33,6 +33,8 @@ CASES = {
     "oddT32": ("xoshiro128starstar", 1 << 21, 1023, "native", "stream"),
     "pmf64": ("xoroshiro128plus", 1 << 20, 1024, "f64", "position"),
     "pm1024": ("xoroshiro1024plusplus", 1 << 20, 1024, "native", "position"),
+    "x1024na": ("xoroshiro1024plusplus", 1 << 20, 1024, "native", "stream", 0, False),
+    "x512na": ("xoshiro512starstar", 1 << 20, 1024, "native", "stream", 0, False),
     "pm32": ("xoshiro128starstar", 1 << 21, 1024, "native", "position"),
     "pmf32": ("xoshiro128starstar", 1 << 21, 1024, "f32", "position"),
     # odd pitch (one element of padding per row): CTA-staged position-major path
@@ -53,6 +55,7 @@ def main():
     for case in a.cases.split(","):
         gen, n, T, kind, layout = CASES[case][:5]
         pad = CASES[case][5] if len(CASES[case]) > 5 else 0
+        adv = CASES[case][6] if len(CASES[case]) > 6 else True  # False: no state write-back
         spec = P.get_spec(gen)
         sub = D.Substreams.from_seed(spec, 42, n)
         out = sub.fill(T, kind=kind, layout=layout)
@@ -64,10 +67,10 @@ def main():
         def timed(target):
             lib.slp_set_fill_pace(target)
             for _ in range(3):
-                sub.fill(T, kind=kind, layout=layout, out=out)
+                sub.fill(T, kind=kind, layout=layout, out=out, advance=adv)
             ev0.record()
             for _ in range(a.launches):
-                sub.fill(T, kind=kind, layout=layout, out=out)
+                sub.fill(T, kind=kind, layout=layout, out=out, advance=adv)
             ev1.record()
             torch.cuda.synchronize()
             return ev0.elapsed_time(ev1) / a.launches
