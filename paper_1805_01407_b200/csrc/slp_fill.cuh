@@ -235,8 +235,15 @@ __global__ void __launch_bounds__(kFillThreads)
       return swz(seg, r, q);
     }
   };
+  // the unit row (substream) this lane generates.  FILL_TMA_G permutes it:
+  // lanes 8q..8q+7 (one shared-memory wavefront of STS.128) take eight rows
+  // of one parity, whose swizzle keys row / g differ; with lane = row the
+  // g rows sharing a key (one per parity) hit the same banks (4-way conflicts
+  // for g = 4, profiles/round2 odd32 ncu capture)
+  int lrow = lane;
+  if constexpr (MODE == FILL_TMA_G) lrow = ((lane & ((32 >> tmap.gsh) - 1)) << tmap.gsh) | (lane >> (5 - tmap.gsh));
   int lead = 0;  // FILL_TMA_G: outputs of this lane's row before its first tile
-  if constexpr (MODE == FILL_TMA_G) lead = tmap.lead[lane & (tmap.g - 1)];
+  if constexpr (MODE == FILL_TMA_G) lead = tmap.lead[lrow & (tmap.g - 1)];
   // FILL_TMA_G, this lane's row: row = lane_row0 + seg * R with R = 32 / g a
   // multiple of 8 (g <= 4, tma_group_ok), so the swizzle key row & 7 is the
   // same for every piece: one multiply-add per chunk instead of recomputing
@@ -244,7 +251,7 @@ __global__ void __launch_bounds__(kFillThreads)
   uint32_t g_lane_row0 = 0, g_rows_per_seg = 0, g_key = 0;
   if constexpr (MODE == FILL_TMA_G) {
     g_rows_per_seg = 32u >> tmap.gsh;
-    g_lane_row0 = (uint32_t)(lane & (tmap.g - 1)) * kSegs * g_rows_per_seg + (uint32_t)(lane >> tmap.gsh);
+    g_lane_row0 = (uint32_t)(lrow & (tmap.g - 1)) * kSegs * g_rows_per_seg + (uint32_t)(lrow >> tmap.gsh);
     g_key = g_lane_row0 & 7u;
   }
 
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(kFillThreads)
   // (the load latency otherwise stalls every warp at each unit start)
   const uint64_t ustride = (uint64_t)gridDim.x * kFillWarps;
   auto load_states = [&](uint64_t unit, word(&dst)[K]) {
-    const uint64_t st = unit * 32 + lane;
+    const uint64_t st = unit * 32 + lrow;
     const bool ok = unit < p.nunits && st < p.nstreams;
 #pragma unroll
     for (int j = 0; j < K; ++j) dst[j] = ok ? sin[j * p.ld + st] : (word)0;
@@ -289,7 +296,7 @@ __global__ void __launch_bounds__(kFillThreads)
   load_states((uint64_t)blockIdx.x * kFillWarps + warp, nxt);
   for (uint64_t u = (uint64_t)blockIdx.x * kFillWarps + warp; u < p.nunits; u += ustride) {
     const uint64_t row0 = u * 32;
-    const uint64_t stream = row0 + lane;
+    const uint64_t stream = row0 + lrow;
     const bool valid = stream < p.nstreams;
     uint64_t pm_roff = 0, pm_col = stream;  // position-major: this lane's segment (row offset, column)
     if constexpr (MODE == FILL_POS || MODE == FILL_POS_TMA) pm_seg(p, stream, pm_roff, pm_col);
@@ -565,7 +572,7 @@ __global__ void __launch_bounds__(kFillThreads)
           const bits x = Cv::conv(eng.next_flat(s));
           if (t < (uint32_t)CH) {
             const uint32_t byte = t * ES;
-            const uint32_t addr = tile + taddr(byte >> 7, lane, (byte & 127) >> 4) + (byte & 15);
+            const uint32_t addr = tile + taddr(byte >> 7, lrow, (byte & 127) >> 4) + (byte & 15);
             if constexpr (ES == 8)
               asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"((uint64_t)x) : "memory");
             else
@@ -591,11 +598,14 @@ __global__ void __launch_bounds__(kFillThreads)
           }
           ++issued;
         }
-        // partial pieces: columns [npieces * CPR, min(rem, CH)) of each row
+        // partial pieces: columns [npieces * CPR, min(rem, CH)) of each row;
+        // pieces below every parity's npieces went out whole by TMA
         const uint32_t lim_w = rem_w < (uint32_t)CH ? rem_w : (uint32_t)CH;
         constexpr int RPP = 32 / CPR;
         const int nseg = (int)((lim_w + CPR - 1) / CPR);
-        for (int r0 = 0; r0 < 32 * nseg; r0 += RPP) {
+        int seg_lo = npieces[0];
+        for (int g = 1; g < tmap.g; ++g) seg_lo = npieces[g] < seg_lo ? npieces[g] : seg_lo;
+        for (int r0 = 32 * seg_lo; r0 < 32 * nseg; r0 += RPP) {
           const int rs = r0 + lane / CPR;  // (piece, row) flattened piece-major
           const int seg = rs / 32, r = rs % 32;
           const int e = lane % CPR;

@@ -587,7 +587,14 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 __device__ __forceinline__ void pace_store(uint64_t &next, uint32_t pace_ns, uint32_t burst) {
   uint64_t now = global_ns();
-  while (now < next) now = global_ns();
+  // sleep through most of the wait: a spinning warp takes issue slots (and
+  // power) from the generating ones (~1/3 of the instructions of a paced
+  // config-2 fill were this loop)
+  while (now < next) {
+    const uint64_t d = next - now;
+    if (d > 128) __nanosleep((uint32_t)(d < 2048 ? d >> 1 : 1024));
+    now = global_ns();
+  }
   now = __shfl_sync(0xffffffffu, now, 0);
   // a warp more than `burst` periods behind its schedule restarts it at now
   next = (now > next + (uint64_t)burst * pace_ns ? now : next) + pace_ns;
