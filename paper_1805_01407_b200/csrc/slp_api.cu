@@ -1058,7 +1058,7 @@ int slp_fill_checksum(int id, const void *states_in, void *states_out, uint64_t 
       if (rc != SLP_OK) return rc;
     }
   }
-  const double fscale = g->w == 64 ? 0x1.0p-53 : 0x1.0p-24;
+  const double fscale = g->w == 64 ? 0x1.0p-64 : 0x1.0p-24;  // fterm in k_fused
   dev::k_fused_final<<<1, 256, 0, st>>>(static_cast<const slp_checksum *>(workspace), grid,
                                         static_cast<slp_checksum *>(result), nstreams * T, fscale);
   return check_launch("k_fused_final");
@@ -1109,7 +1109,7 @@ int slp_fused(int id, const void *states_in, void *states_out, uint64_t ld, uint
     rc = ops->fused(p, flags, st, &grid);
   }
   if (rc != SLP_OK) return rc;
-  const double fscale = g->w == 64 ? 0x1.0p-53 : 0x1.0p-24;
+  const double fscale = g->w == 64 ? 0x1.0p-64 : 0x1.0p-24;  // fterm in k_fused
   dev::k_fused_final<<<1, 256, 0, st>>>(static_cast<const slp_checksum *>(workspace), grid,
                                         static_cast<slp_checksum *>(result), nstreams * T, fscale);
   return check_launch("k_fused_final");

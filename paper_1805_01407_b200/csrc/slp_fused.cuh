@@ -27,6 +27,17 @@ __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedPa
   constexpr int CH = 16;  // multiple of every ring size
   constexpr uint32_t LOWMASK = G::w == 64 ? 0x7FFu : 0xFFu;
   constexpr int SH = G::w == 64 ? 11 : 8;
+  // float64 term of an output, before the final power-of-2 scale
+  // (kFusedF64Scale): for w = 64 the output with its low 11 bits cleared
+  // (2^11 times x >> 11, so every partial sum is exactly 2^11 times the
+  // shifted one and the scaled result is bit-identical) -- one LOP3 on the
+  // low word instead of a two-SHF 64-bit shift
+  auto fterm = [](uint64_t x) -> double {
+    if constexpr (G::w == 64)
+      return __ull2double_rn(x & ~0x7FFull);
+    else
+      return __ull2double_rn(x >> SH);
+  };
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   constexpr int WPB = kFusedThreads / 32;
@@ -112,8 +123,8 @@ __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedPa
 #endif
         xx ^= o0 ^ o1;
         if constexpr (F64) {  // two independent chains: the DADD latency, not the pipe, bounds one chain
-          fs += __ull2double_rn((uint64_t)o0 >> SH);
-          fs2 += __ull2double_rn((uint64_t)o1 >> SH);
+          fs += fterm((uint64_t)o0);
+          fs2 += fterm((uint64_t)o1);
         }
       }
       sx ^= (uint64_t)xx;
@@ -135,7 +146,7 @@ __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedPa
       if constexpr (G::w == 64) acc_hi += (uint32_t)((uint64_t)x >> 32);
       sx ^= (uint64_t)x;
       slow += (uint32_t)x & LOWMASK;
-      if constexpr (F64) fs += __ull2double_rn((uint64_t)x >> SH);
+      if constexpr (F64) fs += fterm((uint64_t)x);
     }
     // fold this substream's exact sum acc_lo + acc_hi * 2^32 into the 128-bit total
     add128(slo, shi, acc_lo2);

@@ -530,8 +530,13 @@ struct Out<SLP_OUT_U64, word> {
 template <class word>
 struct Out<SLP_OUT_F64, word> {
   using bits = uint64_t;
+  // (x >> 11) * 2^-53 computed as (x with its low 11 bits cleared) * 2^-64:
+  // that integer has <= 53 significant bits, so the conversion and the scaling
+  // are both exact and the result is bit-identical, and clearing the bits is
+  // one LOP3 on the low word where the 64-bit shift was two SHF (the f64 fill
+  // is ALU-bound: ncu, profiles/f64_target.py)
   static __device__ __forceinline__ bits conv(word x) {
-    return (uint64_t)__double_as_longlong(__ull2double_rn((uint64_t)x >> 11) * 0x1.0p-53);
+    return (uint64_t)__double_as_longlong(__ull2double_rn((uint64_t)x & ~0x7FFull) * 0x1.0p-64);
   }
 };
 template <class word>
