@@ -141,9 +141,12 @@ def ncu_traffic(kernel_tag):
         return None
 
 
+FUSED_PIPES = "round2_fused_pipes.json"  # profiles/make_fused_pipes.py on the current build
+
+
 def fused_pipes():
     try:
-        with open(os.path.join(ROOT, "profiles", "round1_fused_pipes.json")) as f:
+        with open(os.path.join(ROOT, "profiles", FUSED_PIPES)) as f:
             return json.load(f)
     except OSError:
         return {}
@@ -452,7 +455,7 @@ def run_extra(spec, dev, rank, world):
             res[label]["roofline"] = {"bound": "int (ALU pipe)", "achieved": ach, "peak": peak,
                                       "unit": "warp-inst/s", "frac": round(ach / peak, 4),
                                       "alu_sass_per_output": round(pipes["alu_sass_per_output"], 3),
-                                      "source": "profiles/round1_fused_pipes.json"}
+                                      "source": "profiles/" + FUSED_PIPES}
     # config 5 whole job: 2^34 outputs = 8 long-jump blocks x 2^18 substreams x 2^13,
     # blocks b == rank (mod world), fused exact checksum per GPU, one all_gather
     import torch.distributed as dist
