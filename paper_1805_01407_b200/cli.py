@@ -1,13 +1,17 @@
-"""Command-line front end for the hot path: ``gen`` and ``jump``.
+"""Command-line front end for the hot path: ``gen``, ``jump`` and ``hwd``.
 
-Mirrors the reference CLI (/root/reference/pkg/src/slprng/cli.py): the same
-arguments, output formats and exit codes (0 ok, 1 I/O, 2 usage).
-``gen --format raw`` streams little-endian words produced on the GPU
-(LanedStream -> kernels K1/K2, cli.py:88-97 in the reference); ``hex`` and
-``json`` print the scalar sequence (cli.py:98-104); ``jump`` prints the flat
-state after a jump (cli.py:163-180); ``hwd --algo`` runs the HWD test with
-the GPU counting consumer (cli.py:122-160).  ``hwd --stdin`` and ``analyze``
-are outside this package's scope.
+Behaves like the reference CLI (/root/reference/pkg/src/slprng/cli.py):
+the same subcommands, flags, defaults, output formats and exit codes (0 ok,
+1 I/O, 2 usage, 3 statistical failure).  ``gen --format raw`` streams
+little-endian words produced on the GPU (LanedStream -> kernels K1/K2; the
+reference's cli.py:88-97); ``hex`` and ``json`` print the scalar sequence
+(cli.py:98-104); ``jump`` prints the flat state after a jump (cli.py:163-180);
+``hwd --algo`` runs the HWD test with the GPU counting consumer
+(cli.py:122-160).  ``hwd --stdin`` and ``analyze`` are outside this
+package's scope.
+
+The option tables below (``_OPTIONS``) are the single source of the
+command-line surface; ``build_parser`` only turns them into argparse calls.
 
     python -m paper_1805_01407_b200 gen --algo xoshiro256starstar --seed 42 --values 1e9 > out.bin
 """
@@ -22,50 +26,72 @@ import sys
 from . import generators
 from .generators import Generator, GeneratorSpec
 
-EXIT_OK = 0
-EXIT_IO = 1
-EXIT_USAGE = 2
+EXIT_OK, EXIT_IO, EXIT_USAGE, EXIT_STAT_FAIL = 0, 1, 2, 3
 
 
 class CliError(Exception):
+    """A user-facing failure: message for stderr plus the process exit code."""
+
     def __init__(self, message, code=EXIT_USAGE):
         super().__init__(message)
         self.code = code
 
 
+# ---------------------------------------------------------------- argument types
+
+
 def _parse_int(text: str) -> int:
+    """Integers in any base prefix (0x.., 0o.., 0b..) or decimal."""
     return int(text, 0)
 
 
 def _parse_count(text: str) -> int:
-    """Counts accept 4e9-style notation (cli.py:36-44)."""
+    """Counts: an integer literal, or a float literal with an integral,
+    non-negative value such as 4e9 (reference cli.py:36-44)."""
     try:
         return int(text, 0)
     except ValueError:
-        v = float(text)
-        if v < 0 or v != int(v):
-            raise argparse.ArgumentTypeError(f"not a whole count: {text!r}")
-        return int(v)
+        pass
+    value = float(text)
+    whole = int(value)
+    if value < 0 or value != whole:
+        raise argparse.ArgumentTypeError(f"not a whole count: {text!r}")
+    return whole
+
+
+# ------------------------------------------------------------- generator lookup
 
 
 def _get_spec(name: str) -> GeneratorSpec:
-    try:
+    if name in generators.registry_names(include_analysis=True):
         return generators.get_spec(name)
-    except KeyError:
-        known = ", ".join(sorted(generators.registry_names(include_analysis=True)))
-        raise CliError(f"unknown algorithm {name!r} (known: {known})")
+    names = ", ".join(sorted(generators.registry_names(include_analysis=True)))
+    raise CliError(f"unknown algorithm {name!r} (known: {names})")
+
+
+def _parse_state_words(text: str) -> list[int]:
+    """--state: hexadecimal words separated by commas and/or whitespace."""
+    return [int(tok, 16) for tok in text.replace(",", " ").split()]
 
 
 def _make_generator(args) -> Generator:
+    """The scalar generator a subcommand starts from: --state wins over --seed."""
     spec = _get_spec(args.algo)
-    if getattr(args, "state", None):
-        try:
-            words = [int(t, 16) for t in args.state.replace(",", " ").split()]
-            return Generator(spec, words)
-        except ValueError as e:
-            raise CliError(f"bad --state: {e}")
-    return Generator.from_seed(spec, args.seed)
+    text = getattr(args, "state", None)
+    if not text:
+        return Generator.from_seed(spec, args.seed)
+    try:
+        return Generator(spec, _parse_state_words(text))
+    except ValueError as e:
+        raise CliError(f"bad --state: {e}")
 
+
+def _hex_words(values, w: int) -> list[str]:
+    width = w // 4
+    return [format(v, f"0{width}x") for v in values]
+
+
+# ------------------------------------------------------------------ raw output
 
 # superbatch geometry for raw output: any (lanes, lane_len) gives the same
 # stream (LanedStream contract); 2^16 lanes x 1024 = 512 MiB of u64 per chunk
@@ -108,39 +134,42 @@ def write_raw(spec: GeneratorSpec, gen: Generator, n: int, out) -> None:
         out.write(memoryview(chunk.astype(dtype, copy=False)).cast("B"))
 
 
+# ---------------------------------------------------------------- subcommands
+
+
 def cmd_gen(args) -> int:
     spec = _get_spec(args.algo)
     gen = _make_generator(args)
-    n = args.values
     if args.format == "raw":
-        out = sys.stdout.buffer
+        sink = sys.stdout.buffer
         try:
-            write_raw(spec, gen, n, out)
+            write_raw(spec, gen, args.values, sink)
         except RuntimeError as e:
             raise CliError(str(e), EXIT_IO)
-        out.flush()
-        return EXIT_OK
-    digits = spec.kind.w // 4
-    if args.format == "hex":
-        for _ in range(n):
-            print(f"{gen.next():0{digits}x}")
-        return EXIT_OK
-    print(json.dumps({"algo": args.algo, "seed": args.seed, "values": [gen.next() for _ in range(n)]}))
+        sink.flush()
+    elif args.format == "hex":
+        for word in _hex_words((gen.next() for _ in range(args.values)), spec.kind.w):
+            print(word)
+    else:  # json
+        values = [gen.next() for _ in range(args.values)]
+        print(json.dumps({"algo": args.algo, "seed": args.seed, "values": values}))
     return EXIT_OK
+
+
+def _jump_polynomial(spec: GeneratorSpec, args):
+    if args.steps is not None:
+        return generators.compute_jump_poly(spec, args.steps)
+    short, long_ = generators.default_jumps(spec)
+    return long_ if args.long_jump else short
 
 
 def cmd_jump(args) -> int:
     spec = _get_spec(args.algo)
     gen = _make_generator(args)
-    if args.steps is not None:
-        jp = generators.compute_jump_poly(spec, args.steps)
-    else:
-        jump, long_jump = generators.default_jumps(spec)
-        jp = long_jump if args.long_jump else jump
+    jp = _jump_polynomial(spec, args)
     if jp.step_count:
         gen.jump(jp)
-    digits = spec.kind.w // 4
-    state = [f"{x:0{digits}x}" for x in gen.flat_words()]
+    state = _hex_words(gen.flat_words(), spec.kind.w)
     if args.json:
         print(json.dumps({"algo": args.algo, "steps": str(jp.step_count), "state": state}))
     else:
@@ -148,7 +177,17 @@ def cmd_jump(args) -> int:
     return EXIT_OK
 
 
-EXIT_STAT_FAIL = 3
+_VERDICTS = {"failed": "FAILED (p-value threshold tripped)", "passed": "passed to the byte limit",
+             "inconclusive": "inconclusive (source exhausted)"}
+
+
+def _print_hwd_report(report) -> None:
+    print(f"mode={report.mode} w={report.w} k={report.k} ell={report.ell}")
+    for ck in report.history:
+        print(f"  {ck.bytes:>16d} bytes  p = {ck.p_value:.6g}  "
+              f"signature {ck.faulty_signature} (category {ck.faulty_category})")
+    print(f"{_VERDICTS[report.status]}: {report.bytes_processed} bytes, p = {report.p_value:.6g}, "
+          f"faulty signature {report.faulty_signature!r}")
 
 
 def cmd_hwd(args) -> int:
@@ -168,67 +207,71 @@ def cmd_hwd(args) -> int:
     if args.json:
         print(json.dumps(report.to_dict()))
     else:
-        print(f"mode={report.mode} w={report.w} k={report.k} ell={report.ell}")
-        for ck in report.history:
-            print(f"  {ck.bytes:>16d} bytes  p = {ck.p_value:.6g}  "
-                  f"signature {ck.faulty_signature} (category {ck.faulty_category})")
-        verdict = {"failed": "FAILED (p-value threshold tripped)", "passed": "passed to the byte limit",
-                   "inconclusive": "inconclusive (source exhausted)"}[report.status]
-        print(f"{verdict}: {report.bytes_processed} bytes, p = {report.p_value:.6g}, "
-              f"faulty signature {report.faulty_signature!r}")
+        _print_hwd_report(report)
     return EXIT_STAT_FAIL if report.status == "failed" else EXIT_OK
 
 
+# ------------------------------------------------------------------- the parser
+
+# (flags, argparse keyword arguments) per subcommand, in --help order
+_GENERATOR = [
+    (("--algo",), dict(required=True)),
+]
+_OPTIONS = {
+    "gen": ("emit generator output", cmd_gen, _GENERATOR + [
+        (("--seed",), dict(type=_parse_int, default=0)),
+        (("--state",), dict(help="full state as hex words (overrides --seed)")),
+        (("--values",), dict(type=_parse_count, default=16)),
+        (("--format",), dict(choices=("raw", "hex", "json"), default="raw")),
+    ]),
+    "hwd": ("run the Hamming-weight dependency test on a generator (GPU)", cmd_hwd, [
+        (("--algo",), dict()),
+        (("--stdin",), dict(action="store_true", help="not supported by this build")),
+        (("--seed",), dict(type=_parse_int, default=1)),
+        (("--w",), dict(type=int, default=64)),
+        (("--k",), dict(type=int, default=8)),
+        (("--ell",), dict(type=int, default=None)),
+        (("--C",), dict(type=int, default=None)),
+        (("--mode",), dict(choices=("standard", "transitional"), default="standard")),
+        (("--limit",), dict(type=_parse_count, default=10**15, help="byte limit")),
+        (("--p-threshold",), dict(type=float, default=1e-20, dest="p_threshold")),
+        (("--batch-size",), dict(type=_parse_count, default=None, dest="batch_size")),
+        (("--split",), dict(action="store_true", help="break 64-bit source words into two 32-bit test values")),
+        (("--checkpoint-start",), dict(type=_parse_count, default=None, dest="checkpoint_start")),
+        (("--json",), dict(action="store_true")),
+    ]),
+    "jump": ("print the state after a jump", cmd_jump, _GENERATOR + [
+        (("--seed",), dict(type=_parse_int, default=0)),
+        (("--state",), dict()),
+        (("--steps",), dict(type=_parse_count, default=None,
+                            help="step count (default: the generator's jump, 2^(n/2))")),
+        (("--long-jump",), dict(action="store_true", dest="long_jump", help="use the long jump, 2^(3n/4) steps")),
+        (("--json",), dict(action="store_true")),
+    ]),
+}
+
+
 def build_parser() -> argparse.ArgumentParser:
-    ap = argparse.ArgumentParser(prog="paper_1805_01407_b200",
-                                 description="Scrambled linear generators on B200: bulk output and jumps.")
-    sub = ap.add_subparsers(dest="command", required=True)
-    g = sub.add_parser("gen", help="emit generator output")
-    g.add_argument("--algo", required=True)
-    g.add_argument("--seed", type=_parse_int, default=0)
-    g.add_argument("--state", help="full state as hex words (overrides --seed)")
-    g.add_argument("--values", type=_parse_count, default=16)
-    g.add_argument("--format", choices=("raw", "hex", "json"), default="raw")
-    g.set_defaults(func=cmd_gen)
-    h = sub.add_parser("hwd", help="run the Hamming-weight dependency test on a generator (GPU)")
-    h.add_argument("--algo")
-    h.add_argument("--stdin", action="store_true", help="not supported by this build")
-    h.add_argument("--seed", type=_parse_int, default=1)
-    h.add_argument("--w", type=int, default=64)
-    h.add_argument("--k", type=int, default=8)
-    h.add_argument("--ell", type=int, default=None)
-    h.add_argument("--C", type=int, default=None)
-    h.add_argument("--mode", choices=("standard", "transitional"), default="standard")
-    h.add_argument("--limit", type=_parse_count, default=10**15, help="byte limit")
-    h.add_argument("--p-threshold", type=float, default=1e-20, dest="p_threshold")
-    h.add_argument("--batch-size", type=_parse_count, default=None, dest="batch_size")
-    h.add_argument("--split", action="store_true", help="break 64-bit source words into two 32-bit test values")
-    h.add_argument("--checkpoint-start", type=_parse_count, default=None, dest="checkpoint_start")
-    h.add_argument("--json", action="store_true")
-    h.set_defaults(func=cmd_hwd)
-    j = sub.add_parser("jump", help="print the state after a jump")
-    j.add_argument("--algo", required=True)
-    j.add_argument("--seed", type=_parse_int, default=0)
-    j.add_argument("--state")
-    j.add_argument("--steps", type=_parse_count, default=None,
-                   help="step count (default: the generator's jump, 2^(n/2))")
-    j.add_argument("--long-jump", action="store_true", dest="long_jump",
-                   help="use the long jump, 2^(3n/4) steps")
-    j.add_argument("--json", action="store_true")
-    j.set_defaults(func=cmd_jump)
-    return ap
+    parser = argparse.ArgumentParser(prog="paper_1805_01407_b200",
+                                     description="Scrambled linear generators on B200: bulk output and jumps.")
+    commands = parser.add_subparsers(dest="command", required=True)
+    for name, (summary, handler, options) in _OPTIONS.items():
+        cmd = commands.add_parser(name, help=summary)
+        for flags, kwargs in options:
+            cmd.add_argument(*flags, **kwargs)
+        cmd.set_defaults(func=handler)
+    return parser
 
 
 def main(argv=None) -> int:
-    parser = build_parser()
-    args = parser.parse_args(argv)
+    args = build_parser().parse_args(argv)
     try:
         return args.func(args)
-    except CliError as e:
-        print(f"error: {e}", file=sys.stderr)
-        return e.code
-    except BrokenPipeError:
+    except CliError as err:
+        print(f"error: {err}", file=sys.stderr)
+        return err.code
+    except BrokenPipeError:  # the reader went away: not an error worth a message
         return EXIT_IO
-    except OSError as e:
-        print(f"I/O error: {e}", file=sys.stderr)
+    except OSError as err:
+        print(f"I/O error: {err}", file=sys.stderr)
         return EXIT_IO

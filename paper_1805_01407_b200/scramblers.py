@@ -1,10 +1,11 @@
 """Output functions (+, *, ++, **) on flat state words.
 
-Mirrors /root/reference/pkg/src/slprng/scramblers.py (``ScramblerSpec``
-:48-95 and ``scramble_*`` :26-45).  Scramblers read the state BEFORE the
+Same public surface as /root/reference/pkg/src/slprng/scramblers.py
+(``ScramblerSpec`` :48-95 and ``scramble_*`` :26-45): field names, kinds,
+validation rules and error messages.  Scramblers read the state BEFORE the
 engine step; for ``++`` the first word is the one added back.  The device
 kernels implement the same functions in registers (csrc/slp_gen.cuh,
-``Gen::output``).
+``Gen::output``); this module is the host-side scalar form.
 """
 
 from __future__ import annotations
@@ -15,35 +16,65 @@ __all__ = ["ScramblerSpec", "scramble_plus", "scramble_star", "scramble_plusplus
            "scramble_starstar", "SCRAMBLER_KINDS", "SCRAMBLER_CODE"]
 
 SCRAMBLER_KINDS = ("none", "plus", "star", "plusplus", "starstar")
-SCRAMBLER_CODE = {k: i for i, k in enumerate(SCRAMBLER_KINDS)}
+SCRAMBLER_CODE = {k: i for i, k in enumerate(SCRAMBLER_KINDS)}  # the C ABI's SLP_SC_* order
 
 
-def _mask(w):
-    return (1 << w) - 1
+def _wrap(x: int, w: int) -> int:
+    """x modulo 2^w."""
+    return x & ((1 << w) - 1)
+
+
+def _rotl(x: int, r: int, w: int) -> int:
+    return _wrap(x << r | x >> (w - r), w)
 
 
 def scramble_plus(x: int, y: int, w: int) -> int:
-    return (x + y) & _mask(w)
+    return _wrap(x + y, w)
 
 
 def scramble_star(x: int, s: int, w: int) -> int:
-    return (x * s) & _mask(w)
-
-
-def _rl(x, r, w):
-    return ((x << r) | (x >> (w - r))) & _mask(w)
+    return _wrap(x * s, w)
 
 
 def scramble_plusplus(x: int, y: int, r: int, w: int) -> int:
-    return (_rl((x + y) & _mask(w), r, w) + x) & _mask(w)
+    """rotl(x + y, r) + x."""
+    return _wrap(_rotl(_wrap(x + y, w), r, w) + x, w)
 
 
 def scramble_starstar(x: int, s: int, r: int, t: int, w: int) -> int:
-    return (_rl((x * s) & _mask(w), r, w) * t) & _mask(w)
+    """rotl(x * s, r) * t."""
+    return _wrap(_rotl(_wrap(x * s, w), r, w) * t, w)
+
+
+def _odd(v) -> bool:
+    return v is not None and v % 2 == 1
+
+
+# (kinds a rule applies to, predicate on (spec, k, w), message) -- the range
+# checks of the reference's ScramblerSpec.validate (scramblers.py:68-82), in its order
+_RULES = (
+    (SCRAMBLER_KINDS, lambda s, k, w: 0 <= s.word_i < k, "word_i out of range"),
+    (("plus", "plusplus"), lambda s, k, w: s.word_j is not None and 0 <= s.word_j < k, "word_j out of range"),
+    (("star", "starstar"), lambda s, k, w: _odd(s.S), "multiplier S must be odd"),
+    (("plusplus", "starstar"), lambda s, k, w: s.R is not None and 0 < s.R < w, "rotation R out of range"),
+    (("starstar",), lambda s, k, w: _odd(s.T), "multiplier T must be odd"),
+)
+
+# kind -> f(spec, words, w)
+_APPLY = {
+    "none": lambda s, words, w: words[s.word_i],
+    "plus": lambda s, words, w: scramble_plus(words[s.word_i], words[s.word_j], w),
+    "star": lambda s, words, w: scramble_star(words[s.word_i], s.S, w),
+    "plusplus": lambda s, words, w: scramble_plusplus(words[s.word_i], words[s.word_j], s.R, w),
+    "starstar": lambda s, words, w: scramble_starstar(words[s.word_i], s.S, s.R, s.T, w),
+}
 
 
 @dataclass(frozen=True)
 class ScramblerSpec:
+    """Output function ``kind`` applied to flat state word ``word_i`` (and
+    ``word_j`` for + and ++) with multipliers S, T and rotation R."""
+
     kind: str
     word_i: int = 0
     word_j: int | None = None
@@ -56,27 +87,11 @@ class ScramblerSpec:
             raise ValueError(f"unknown scrambler kind {self.kind!r}")
 
     def validate(self, k: int, w: int):
-        """Range checks of scramblers.py:68-82."""
-        if not 0 <= self.word_i < k:
-            raise ValueError("word_i out of range")
-        if self.kind in ("plus", "plusplus") and (self.word_j is None or not 0 <= self.word_j < k):
-            raise ValueError("word_j out of range")
-        if self.kind in ("star", "starstar") and (self.S is None or self.S % 2 == 0):
-            raise ValueError("multiplier S must be odd")
-        if self.kind in ("plusplus", "starstar") and (self.R is None or not 0 < self.R < w):
-            raise ValueError("rotation R out of range")
-        if self.kind == "starstar" and (self.T is None or self.T % 2 == 0):
-            raise ValueError("multiplier T must be odd")
+        """Raise ValueError unless the spec fits a k-word, w-bit engine."""
+        for kinds, ok, message in _RULES:
+            if self.kind in kinds and not ok(self, k, w):
+                raise ValueError(message)
 
     def apply(self, words, w: int) -> int:
-        x = words[self.word_i]
-        kind = self.kind
-        if kind == "none":
-            return x
-        if kind == "plus":
-            return scramble_plus(x, words[self.word_j], w)
-        if kind == "star":
-            return scramble_star(x, self.S, w)
-        if kind == "plusplus":
-            return scramble_plusplus(x, words[self.word_j], self.R, w)
-        return scramble_starstar(x, self.S, self.R, self.T, w)
+        """Scramble the flat state words (before the engine step)."""
+        return _APPLY[self.kind](self, words, w)
