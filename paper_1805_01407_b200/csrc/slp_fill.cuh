@@ -765,22 +765,22 @@ constexpr int kPm2Pos = 64;
 constexpr int kPm2TileBytes = kPm2Pos * 64 * 4;
 
 // store pacing period (pace_store): `units` units of work spread over `agents`
-// (warps or CTAs) that each store `tiles_per_unit` tiles of `tile_bytes` per
-// unit; the whole fill should take bytes / fill_pace_gbps (bytes per ns), and
-// the busiest agent stores ceil(units / agents) x tiles_per_unit tiles in that
-// time.  0 = unpaced.
-// Position-major tiles (8 MiB-apart rows of 256 B) and the 1024-bit engine
-// (16-word states read and written around every unit) congest earlier: each
-// is paced at 95% of the target (measured best at ~6200 where stream-major
-// rows of the small engines are best at 6500, profiles/round2_pace_*.jsonl).
+// (warps) that each store `tiles_per_unit` tiles of `tile_bytes` per unit and
+// read / write `state_bytes` of substream states per unit.  The target rate
+// (fill_pace_gbps) is in bytes of output + 1.5 x bytes of state traffic per
+// ns: state reads mixed into the write stream cost about 1.5x their bytes
+// (best paced rates measured for rows of 64, 128 and 1024 outputs and the
+// 16-word xoroshiro1024 states all fit that, profiles/round2_pace_short.jsonl,
+// round2_pace_x.jsonl).  Position-major tiles (8 MiB-apart rows of 256 B)
+// congest earlier and are paced at 95% of it.  The busiest agent stores
+// ceil(units / agents) x tiles_per_unit tiles in the target time.  0 = unpaced.
 inline uint32_t pace_period_ns(uint64_t units, uint64_t agents, uint64_t tiles_per_unit, uint64_t tile_bytes,
-                               bool position_major = false, bool wide_state = false) {
+                               uint64_t state_bytes, bool position_major = false) {
   int gbps = fill_pace_gbps();
   if (position_major) gbps = gbps * 95 / 100;
-  if (wide_state) gbps = gbps * 95 / 100;
   if (gbps <= 0 || !units || !agents || !tiles_per_unit) return 0;
   const uint64_t tiles_max = (units + agents - 1) / agents * tiles_per_unit;
-  const double ns = (double)units * tiles_per_unit * tile_bytes / gbps;
+  const double ns = (double)units * ((double)tiles_per_unit * tile_bytes + 1.5 * (double)state_bytes) / gbps;
   return (uint32_t)(ns / (double)tiles_max);
 }
 constexpr int kPm2Smem = kFillWarps * 2 * kPm2TileBytes + 1024;
@@ -884,7 +884,8 @@ int launch_fill_pm2(const FillParams &p, cudaStream_t st) {
   const uint64_t cap = (uint64_t)sm_count(dev) * fill_grid_mult();
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   FillParams q = p;
-  q.pace_ns = pace_period_ns(nunits, (uint64_t)grid * kFillWarps, p.T / kPm2Pos, kPm2TileBytes, true);
+  q.pace_ns = pace_period_ns(nunits, (uint64_t)grid * kFillWarps, p.T / kPm2Pos, kPm2TileBytes,
+                             64ull * G::k * sizeof(typename G::word) * (p.sout ? 2 : 1), true);
   q.pace_burst = (uint32_t)fill_pace_burst();
   kern<<<grid, kFillThreads, kPm2Smem, st>>>(q, tmap);
   return check_launch("k_fill_pm2");
@@ -1107,7 +1108,7 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
   if constexpr (!CSUM && (MODE == FILL_TMA || MODE == FILL_POS_TMA || (MODE == FILL_TMA_G && ES == 8))) {
     const uint64_t tiles_per_unit = (p.T + Shape::row_bytes / ES - 1) / (Shape::row_bytes / ES);
     p.pace_ns = pace_period_ns(p.nunits, (uint64_t)grid * kFillWarps, tiles_per_unit, Shape::tile_bytes,
-                               MODE == FILL_POS_TMA, G::k * G::w >= 1024);
+                               32ull * G::k * sizeof(typename G::word) * (p.sout ? 2 : 1), MODE == FILL_POS_TMA);
     p.pace_burst = (uint32_t)fill_pace_burst();
     static const bool no_store = std::getenv("SLP_FILL_NO_STORE") != nullptr;
     p.no_store = no_store;

@@ -101,9 +101,10 @@ struct TableJumpParams {
 #define SLP_FILL_WARPS 7
 #endif
 constexpr int kFillWarps = SLP_FILL_WARPS;
-// default store-pacing target of the TMA fill modes in GB/s (0 = unpaced)
+// default store-pacing target of the TMA fill modes in GB/s of output + 1.5 x
+// state traffic (0 = unpaced; pace_period_ns in slp_fill.cuh)
 #ifndef SLP_DEFAULT_PACE_GBPS
-#define SLP_DEFAULT_PACE_GBPS 6500
+#define SLP_DEFAULT_PACE_GBPS 6600
 #endif
 constexpr int kDefaultPaceGbps = SLP_DEFAULT_PACE_GBPS;
 

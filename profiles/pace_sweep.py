@@ -28,6 +28,9 @@ CASES = {
     "x512": ("xoshiro512starstar", 1 << 20, 1024, "native", "stream"),
     "x1024": ("xoroshiro1024plusplus", 1 << 20, 1024, "native", "stream"),
     "pm": ("xoshiro256starstar", 1 << 20, 1024, "native", "position"),
+    "t64": ("xoshiro256starstar", 1 << 24, 64, "native", "stream"),
+    "t128": ("xoshiro256starstar", 1 << 23, 128, "native", "stream"),
+    "t256": ("xoshiro256starstar", 1 << 22, 256, "native", "stream"),
     "t2048": ("xoshiro256starstar", 1 << 19, 2048, "native", "stream"),
     "oddT": ("xoshiro256starstar", 1 << 20, 1023, "native", "stream"),
     "oddT32": ("xoshiro128starstar", 1 << 21, 1023, "native", "stream"),
