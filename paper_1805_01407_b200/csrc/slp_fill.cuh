@@ -268,9 +268,6 @@ __global__ void __launch_bounds__(kFillThreads)
   const uint64_t rem = p.T - ntiles * CH;
   uint32_t issued = 0;  // tiles produced by this warp
   uint64_t pace_next = 0;  // store pacing: earliest issue time (global ns) of this warp's next tile store
-#ifdef SLP_FILL_DBG_NOSTS
-  uint64_t dbg_sink = 0;
-#endif
   uint64_t cs_lo = 0, cs_hi = 0, cs_x = 0, cs_low = 0;  // CSUM accumulators (zero states emit zeros)
 
   // the next unit's start states are loaded while this unit is generated
@@ -333,13 +330,6 @@ __global__ void __launch_bounds__(kFillThreads)
       // one 16-byte chunk (outputs b+e .. b+e+EPC-1 of this lane's row) into the
       // tile; b (runtime) is a sub-block start, e (compile time) the offset in it
       auto put = [&](uint32_t b, int e, const bits(&v)[EPC]) {
-#ifdef SLP_FILL_DBG_NOSTS  // measurement builds only: generation without the shared stores
-        if constexpr (MODE == FILL_TMA) {
-#pragma unroll
-          for (int i = 0; i < EPC; ++i) dbg_sink ^= (uint64_t)v[i];
-          return;
-        }
-#endif
         if constexpr (MODE == FILL_POS_TMA) {  // tile [position][lane]
           const uint32_t row = tile + (b * 32 + lane) * ES;
 #pragma unroll
@@ -748,9 +738,6 @@ __global__ void __launch_bounds__(kFillThreads)
     if (elect_one()) bulk_wait_all<0>();
   }
   if constexpr (CSUM) reduce_checksum_block<kFillWarps>(cs_lo, cs_hi, cs_x, cs_low, 0.0, p.partials);
-#ifdef SLP_FILL_DBG_NOSTS
-  if (dbg_sink == 0x0123456789abcdefull) out[0] = (bits)dbg_sink;
-#endif
 }
 
 
