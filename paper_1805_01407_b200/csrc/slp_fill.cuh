@@ -465,9 +465,10 @@ __global__ void __launch_bounds__(kFillThreads)
         if (p.pace_ns) pace_store(pace_next, p.pace_ns, p.pace_burst);
         __syncwarp();
         if (elect_one()) {
-          if (!p.no_store)
-            tma_store_4d(&tmap, tile, 0, (int)(row0 & ((1ull << p.jsh) - 1)), (int)(row0 >> p.jsh),
-                         (int)(pos0 * ES / 128));
+#ifndef SLP_MEASURE_NO_STORE  // variant builds only: generation without the stores (profiles/nostore_probe.py)
+          tma_store_4d(&tmap, tile, 0, (int)(row0 & ((1ull << p.jsh) - 1)), (int)(row0 >> p.jsh),
+                       (int)(pos0 * ES / 128));
+#endif
           bulk_commit();
         }
         ++issued;
@@ -1097,8 +1098,6 @@ int launch_fill(const FillParams &p0, cudaStream_t st, int *grid_out = nullptr) 
     p.pace_ns = pace_period_ns(p.nunits, (uint64_t)grid * kFillWarps, tiles_per_unit, Shape::tile_bytes,
                                32ull * G::k * sizeof(typename G::word) * (p.sout ? 2 : 1), MODE == FILL_POS_TMA);
     p.pace_burst = (uint32_t)fill_pace_burst();
-    static const bool no_store = std::getenv("SLP_FILL_NO_STORE") != nullptr;
-    p.no_store = no_store;
   }
   kern<<<grid, kFillThreads, smem, st>>>(p, tmap);
   return check_launch("k_fill");

@@ -43,7 +43,6 @@ struct FillParams {
   // stores, set by the launcher from the target rate (0 = unpaced)
   uint32_t pace_ns;
   uint32_t pace_burst;  // periods a late warp may catch up (pace_store)
-  uint32_t no_store;  // measurement only (SLP_FILL_NO_STORE=1): generate tiles, skip the TMA stores
 };
 
 struct FusedParams {

@@ -1,10 +1,12 @@
 """Is k_fill store-bound or generation-bound?  Times the fill of BASELINE
-config shapes with and without the TMA stores (SLP_FILL_NO_STORE=1 in the
-environment: tiles are generated into shared memory and dropped), with the
-median SM clock during the timed launches (NVML).
+config shapes with and without the TMA stores, with the median SM clock
+during the timed launches (NVML).  The store-less kernel is a variant build
+(round 2 measured it through an environment switch, since removed so that
+no run-time setting can drop stores):
 
+  make variant VARIANT=nostore EXTRA=-DSLP_MEASURE_NO_STORE
   python profiles/nostore_probe.py [cases] [launches]
-  SLP_FILL_NO_STORE=1 python profiles/nostore_probe.py ...
+  SLP_LIB=variants/libslp_nostore.so python profiles/nostore_probe.py ...
 """
 import json
 import os
@@ -56,7 +58,7 @@ def main():
         th.join()
         ms = ev0.elapsed_time(ev1) / launches
         clocks.sort()
-        print(json.dumps({"case": case, "no_store": os.environ.get("SLP_FILL_NO_STORE") is not None,
+        print(json.dumps({"case": case, "lib": os.environ.get("SLP_LIB", "in-tree"),
                           "pace_gbps": P._native.lib().slp_set_fill_pace(-1), "ms": round(ms, 4),
                           "GBps_equiv": round(nbytes / ms / 1e6, 1),
                           "sm_mhz_median": clocks[len(clocks) // 2] if clocks else None}), flush=True)
