@@ -344,7 +344,9 @@ def _totals_async(counter, group):
     if group is not None:
         import torch.distributed as dist
 
-        dist.all_reduce(both, op=dist.ReduceOp.SUM, group=group)
+        # torch's NCCL group rejects uint64; the int64 view sums the same bits
+        # (two's complement addition is the same modulo 2^64)
+        dist.all_reduce(both.view(torch.int64), op=dist.ReduceOp.SUM, group=group)
     n = cnt.numel()
     if not both.is_cuda:
         host = both.numpy().view(np.uint64)
