@@ -35,7 +35,9 @@ def _worker(port, q, c5, hwd_case):
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
     try:
-        dist.init_process_group("nccl", rank=0, world_size=1)
+        # as bench.py initialises it (device_id binds the communicator eagerly)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        dist.barrier()
         import paper_1805_01407_b200 as P
         from paper_1805_01407_b200 import hwd
         from paper_1805_01407_b200.multigpu import _device_compute, collective_device, gather_checksums
