@@ -231,7 +231,13 @@ int make_store_tmap_pm(CUtensorMap *map, void *out, int es, uint64_t T, uint64_t
 // (odd T: 4.2-4.9 TB/s against 3.8-4.3 with 16-byte alignment); 16 bytes for
 // 4-byte outputs, where sector alignment needs g = 8 rows of 4 per box and
 // measured slower (profiles/round1_ragged.jsonl).
-static uint64_t row_align(int es) { return es == 8 ? 32 : 16; }
+// row-group TMA: rows start on a 32-byte sector (8-byte outputs: g <= 4) or
+// 16 bytes (4-byte outputs); SLP_ROW_ALIGN64=16 (A/B) aligns 8-byte rows to
+// 16 bytes (g <= 2: half the boxes per tile, partial sectors at the edges)
+static uint64_t row_align(int es) {
+  static const int a64 = env_int("SLP_ROW_ALIGN64", 32) == 16 ? 16 : 32;
+  return es == 8 ? (uint64_t)a64 : 16;
+}
 static uint64_t row_group(uint64_t pitch_bytes, int es) {  // row_align / gcd(pitch, row_align)
   const uint64_t a = row_align(es);
   uint64_t g = 1;
