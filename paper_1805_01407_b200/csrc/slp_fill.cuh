@@ -283,8 +283,11 @@ __global__ void __launch_bounds__(kFillThreads)
   // of the tile whose first piece is piece0 (counted after each row's lead)
   auto store_groups = [&](uint32_t tile, uint64_t row0, uint64_t piece0, const int *npieces) {
     if constexpr (MODE == FILL_TMA_G) {
-      for (int g = 0; g < tmap.g; ++g)
-        if (!npieces || npieces[g] > 0)
+      // unrolled to the maximum g (4): each store gets its own uniform
+      // registers, so no store waits for the previous one to read its operands
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (g < tmap.g && (!npieces || npieces[g] > 0))
           tma_store_3d(&tmap.m[g], tile + ((g * kSegs * (32 >> tmap.gsh)) << 7), 0, (int)(row0 >> tmap.gsh),
                        (int)piece0);
     }
