@@ -223,11 +223,13 @@ int slp_hwd_count(int id, const void *states, uint64_t ld, uint64_t nthreads, ui
  * per device, built and freed stream-ordered (no host synchronisation). */
 size_t slp_device_cache_bytes(int device);
 /* Store pacing of the TMA fill paths (no reference counterpart; a tuning
- * knob): the fill kernels offer their tile stores at no more than `gbps` GB/s
- * in aggregate, because HBM sustains a paced stream of row-piece stores
- * faster than an unpaced one (profiles/round2_pacing.md).
- * 0 disables pacing, a negative value only queries.  Returns the previous
- * target.  Default: SLP_FILL_PACE_GBPS, else the built-in target. */
+ * knob that never changes results): the fill kernels offer their tile stores
+ * at no more than `gbps` GB/s in aggregate, counted as output bytes plus 1.5x
+ * the substream-state bytes read and written, because HBM sustains a paced
+ * stream of row-piece stores faster than an unpaced one (DESIGN.md §4,
+ * profiles/round2_pacing.md).  0 disables pacing, a negative value only
+ * queries.  Returns the previous target.  Default: SLP_FILL_PACE_GBPS, else
+ * the built-in 6600. */
 int slp_set_fill_pace(int gbps);
 const char *slp_status_str(int status);
 /* last CUDA error string seen by this thread ("" if none) */
