@@ -46,14 +46,15 @@ def test_substreams_and_fill(name):
     np.testing.assert_array_equal(sub.states_numpy().astype(np.uint64), want_S)
 
 
-@pytest.mark.parametrize("name", DEVICE)
-@pytest.mark.parametrize("kind", ["native", "u64", "f64", "f32"])
+def kinds_of(w):
+    """Output kinds defined for a word width (zero-extended u64 only for w = 32)."""
+    return ["native", "f64"] if w == 64 else ["native", "u64", "f32"]
+
+
+@pytest.mark.parametrize("name,kind", [(n, k) for n in DEVICE for k in kinds_of(CUSTOM[n]["w"])])
 @pytest.mark.parametrize("layout", ["stream", "position"])
 def test_fill_kinds_layouts(name, kind, layout):
     spec = spec_of(name)
-    w = spec.kind.w
-    if (kind == "f64" and w != 64) or (kind == "f32" and w != 32) or (kind == "u64" and w == 64):
-        pytest.skip("kind not defined for this width")
     rng = np.random.default_rng(len(name))
     n, T = int(rng.integers(33, 300)), int(rng.integers(17, 700))
     sub = D.Substreams.from_seed(spec, 7, n)

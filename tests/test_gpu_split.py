@@ -91,19 +91,17 @@ def test_split_rates_lift_the_cliff():
         assert tbs > 0.5, (args.get("layout", "stream"), tbs)
 
 
-@pytest.mark.parametrize("name", ["xoshiro256starstar", "xoroshiro128plus", "xoroshiro1024starstar",
-                                  "xoshiro128starstar", "xoroshiro64starstar"])
+@pytest.mark.parametrize("name,kind", [(n, k) for n in ["xoshiro256starstar", "xoroshiro128plus", "xoroshiro1024starstar",
+                                                        "xoshiro128starstar", "xoroshiro64starstar"]
+                                       for k in ["native", "float"] + (["u64"] if P.get_spec(n).kind.w == 32 else [])])
 @pytest.mark.parametrize("n,T,pad,off", [(225, 70, 0, 0), (1001, 64, 2, 1), (449, 33, 1, 3), (3, 100, 0, 1),
                                          (672, 96, 5, 2), (7, 5, 0, 0)])
-@pytest.mark.parametrize("kind", ["native", "float", "u64"])
 def test_position_major_unaligned_rows(name, n, T, pad, off, kind):
     """Rows no TMA map can address (odd pitch / unaligned base): the
     CTA-staged path (k_fill_pos_cta: sector-aligned bulk interiors, element
     stores at the CTA edges) -- partial CTA blocks, partial tiles, padding."""
     spec = P.get_spec(name)
     w = spec.kind.w
-    if kind == "u64" and w == 64:
-        pytest.skip("u64 is native for w = 64")
     k = ("f64" if w == 64 else "f32") if kind == "float" else kind
     dt = {("native", 64): torch.uint64, ("native", 32): torch.uint32, ("f64", 64): torch.float64,
           ("f32", 32): torch.float32, ("u64", 32): torch.uint64}[(k, w)]
