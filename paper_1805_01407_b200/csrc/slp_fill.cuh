@@ -202,6 +202,29 @@ __device__ __forceinline__ void reduce_checksum_block(uint64_t slo, uint64_t shi
   }
 }
 
+// FMA-form site mask of the generator inside k_fill (even / odd outputs).
+// Build knobs for A/B: SLP_FILL_MASK[2] (every kind), SLP_FILLC_MASK[2]
+// (converted and store + checksum kinds only: the generation-bound ones).
+template <class G, int OK, bool CSUM>
+__host__ __device__ constexpr int fill_site_mask(int odd) {
+  int m = G::best_mask(0, 0), m2 = m;
+#ifdef SLP_FILL_MASK
+  m = m2 = SLP_FILL_MASK;
+#ifdef SLP_FILL_MASK2
+  m2 = SLP_FILL_MASK2;
+#endif
+#endif
+#ifdef SLP_FILLC_MASK
+  if (CSUM || OK != SLP_OUT_NATIVE) {
+    m = m2 = SLP_FILLC_MASK;
+#ifdef SLP_FILLC_MASK2
+    m2 = SLP_FILLC_MASK2;
+#endif
+  }
+#endif
+  return (odd ? m2 : m) & G::kSites;
+}
+
 template <class G, int OK, int MODE, bool CSUM = false, bool SHORT = false, bool TAIL = false>
 __global__ void __launch_bounds__(kFillThreads)
     k_fill(FillParams p, const __grid_constant__ typename FillTmap<MODE>::type tmap) {
@@ -222,7 +245,8 @@ __global__ void __launch_bounds__(kFillThreads)
   static_assert(!G::ring || U % K == 0, "sub-blocks must cover whole ring periods");
   // 16-byte chunks produced before the buffer wait (at most one sub-block)
   constexpr int PRE = MODE == FILL_POS ? 0 : (Shape::pre * EPC <= U ? Shape::pre : U / EPC);
-  constexpr int MSK = G::best_mask(0, 0);  // rotation pipe mix (ALU vs FMA), see Gen::best_mask
+  // pipe mix of the generator's sites (ALU vs FMA forms, Gen::kSites); MSK2 = odd outputs
+  constexpr int MSK = fill_site_mask<G, OK, CSUM>(0), MSK2 = fill_site_mask<G, OK, CSUM>(1);
   const int lane = threadIdx.x & 31;
   const int warp = warp_uniform();  // keeps TMA coordinates in uniform registers
   // shared-tile address of chunk q of piece seg of unit row r: [seg][row] or,
@@ -372,9 +396,14 @@ __global__ void __launch_bounds__(kFillThreads)
 #pragma unroll
         for (int i = 0; i < EPC; ++i) {
           const int o = (e + i) % K;
-          rr[i] = eng.template output_m<MSK>(s, o);
+          if ((i & 1) == 0) {  // folded after unrolling
+            rr[i] = eng.template output_m<MSK>(s, o);
+            eng.template step_m<MSK>(s, o);
+          } else {
+            rr[i] = eng.template output_m<MSK2>(s, o);
+            eng.template step_m<MSK2>(s, o);
+          }
           v[i] = Cv::conv(rr[i]);
-          eng.template step_m<MSK>(s, o);
         }
         if constexpr (CSUM) {
           constexpr uint32_t LOWM = G::w == 64 ? 0x7FFu : 0xFFu;

@@ -16,6 +16,23 @@ namespace dev {
 
 constexpr int kFusedThreads = 256;
 
+// FMA-form sites of the generator inside K4 (Gen::kSites).  Measured
+// (profiles/round2_ab_fused_sites.md): only plain IMAD overlaps with the ALU
+// pipe -- IMAD.HI and IMAD.WIDE add to its time (profiles/int_peak.cu mixes)
+// -- so rotations and shifts stay ALU forms (every FMA form lost 1-25%).  The
+// scrambler multiplies do better as IMAD + IMAD + IMAD.HI (site 16) than as
+// IMAD.WIDE + IMAD: +1..4%, except the two cases below (-1%).
+template <class G, bool MANT, bool F64>
+__host__ __device__ constexpr int fused_site_mask() {
+  if constexpr (G::runtime || !(G::kSites & 16)) {
+    return G::best_mask(1, (G::w == 64 ? 2 : 1) + (MANT ? 1 : 0));
+  } else {
+    if (G::fam == SLP_FAM_XOSHIRO && G::k == 8 && !MANT) return 0;                                // xoshiro512**, sum + xor
+    if (G::fam == SLP_FAM_XOROSHIRO && G::k == 16 && G::sc == SLP_SC_STARSTAR && !F64) return 0;  // xoroshiro1024**
+    return 16;
+  }
+}
+
 template <class G, bool MANT, bool F64>
 #ifndef SLP_FUSED_MINB
 #define SLP_FUSED_MINB 1
@@ -52,10 +69,16 @@ __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedPa
   // is an opaque 1 from the parameters so ptxas cannot turn it into IADD3);
   // together they give the EXACT sum.  xor: one 3-input LOP3 per output pair
   // and half.  MANT: low-bit sum = LOP3 + IMAD.
-#ifdef SLP_FUSED_MASK  // A/B: force the FMA-form rotation sites (masked to the generator's sites)
+#ifdef SLP_FUSED_MASK  // A/B: force the FMA-form sites (masked to the generator's sites); MASK2: odd outputs
   constexpr int MSK = SLP_FUSED_MASK & G::kSites;
+#ifdef SLP_FUSED_MASK2
+  constexpr int MSK2 = SLP_FUSED_MASK2 & G::kSites;
 #else
-  constexpr int MSK = G::best_mask(G::w == 64 ? 1 : 1, (G::w == 64 ? 2 : 1) + (MANT ? 1 : 0));
+  constexpr int MSK2 = MSK;
+#endif
+#else
+  constexpr int MSK = fused_site_mask<G, MANT, F64>();
+  constexpr int MSK2 = MSK;
 #endif
   const uint32_t one = p.one;
   uint64_t slo = 0, shi = 0, sx = 0, slow = 0;
@@ -75,8 +98,8 @@ __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedPa
       for (int t = 0; t < CH; t += 2) {
         const word o0 = eng.template output_m<MSK>(s, t % K);
         eng.template step_m<MSK>(s, t % K);
-        const word o1 = eng.template output_m<MSK>(s, (t + 1) % K);
-        eng.template step_m<MSK>(s, (t + 1) % K);
+        const word o1 = eng.template output_m<MSK2>(s, (t + 1) % K);
+        eng.template step_m<MSK2>(s, (t + 1) % K);
 #if SLP_SUM_POLICY == 2
         // separate even/odd accumulators: one IMAD.WIDE per chain per pair,
         // nothing for ptxas to re-associate into IADD3

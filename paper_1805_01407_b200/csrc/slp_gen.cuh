@@ -65,7 +65,7 @@ __device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {
 //   shl    : IMAD.SHL (low half) + SHF.L.U64.HI          -> 1 FMA + 1 ALU
 //   mulc   : IMAD.WIDE + IMAD (+ IMAD for a 64-bit constant).
 #ifndef SLP_ROTH_FORM
-#define SLP_ROTH_FORM 1  // rotl_h low halves: 1 constant shifts, 0 mul.lo by an opaque 2^r
+#define SLP_ROTH_FORM 0  // rotl_h low halves: 1 constant shifts + mad.hi, 0 mul.hi + mad.lo by an opaque 2^r
 #endif
 #ifndef SLP_MUL_POLICY
 #define SLP_MUL_POLICY 1  // 0: shifts via IMAD.WIDE; 1: 64-bit constant shifts as IMAD.SHL + SHF; 2: also x*(2^a+1) as LEA pairs
@@ -99,6 +99,15 @@ struct WOps<32> {
   }
   template <unsigned long long C>
   static __device__ __forceinline__ word mulc(word x) {
+    return x * (uint32_t)C;
+  }
+  template <int B>
+  static __device__ __forceinline__ word shl_h(word x, uint32_t) {
+    return x << B;
+  }
+  static __device__ __forceinline__ word add_x(word a, word b, uint32_t) { return a + b; }
+  template <unsigned long long C>
+  static __device__ __forceinline__ word mulc_h(word x, uint32_t) {
     return x * (uint32_t)C;
   }
 };
@@ -155,16 +164,20 @@ struct WOps<64> {
     if constexpr ((R & 31) == 0) return pack(l, h);
     constexpr int r = R & 31;
 #if SLP_ROTH_FORM == 1
+    // constant shifts (SHF or IMAD.SHL, ptxas's choice) + mad.hi: the SASS
+    // IMAD.HI addend is a 64-bit pair, so each mad.hi also costs an IMAD.MOV
     const uint32_t ll = l << r, hl = h << r;
     (void)m2;
-#else
-    uint32_t ll, hl;
-    asm("mul.lo.u32 %0, %1, %2;" : "=r"(ll) : "r"(l), "r"(m2));
-    asm("mul.lo.u32 %0, %1, %2;" : "=r"(hl) : "r"(h), "r"(m2));
-#endif
     uint32_t nl, nh;
     asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(nl) : "r"(h), "r"(m), "r"(ll));
     asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(nh) : "r"(l), "r"(m), "r"(hl));
+#else
+    // FMA pipe only: IMAD.HI (no addend) + IMAD by a second opaque 2^r
+    uint32_t ch, cl;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(ch) : "r"(h), "r"(m));
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(cl) : "r"(l), "r"(m));
+    const uint32_t nl = madlo(l, m2, ch), nh = madlo(h, m2, cl);
+#endif
     return pack(nl, nh);
   }
   template <int B>
@@ -196,6 +209,47 @@ struct WOps<64> {
     uint32_t h = madlo(hi(x), (uint32_t)C, (uint32_t)(p >> 32));
     if constexpr ((C >> 32) != 0) h = madlo(lo(x), (uint32_t)(C >> 32), h);
     return pack((uint32_t)p, h);
+  }
+  // FMA-pipe forms for kernels whose ALU pipe is the bound (K4).  The carry
+  // into the high word is hi32(lo * m) with m in a register ptxas cannot see
+  // through: one half-rate IMAD.HI (no addend: SASS IMAD.HI adds a 64-bit
+  // register pair, so a PTX mad.hi addend costs a MOV) where shl spends an ALU
+  // SHF.L.U64.HI and mulc a quarter-rate IMAD.WIDE.  The halves are split
+  // with mov.b64 so that NVVM does not re-combine (x >> 32) << B into a
+  // 64-bit shift plus mask.
+  static __device__ __forceinline__ void split(word x, uint32_t &l, uint32_t &h) {
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(l), "=r"(h) : "l"(x));
+  }
+  static __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+  }
+  // 64-bit add with the high word on the FMA pipe: IADD3 (carry out) +
+  // IMAD.X (hi(a) * one + hi(b) + carry; `one` opaque so it stays an IMAD)
+  // instead of IADD3 + IADD3.X.  Plain IMADs run beside ALU instructions
+  // (profiles/int_peak.cu mixes), so the add costs one ALU slot, not two.
+  static __device__ __forceinline__ word add_x(word a, word b, uint32_t one) {
+    uint32_t l, h;
+    asm("add.cc.u32 %0, %2, %4;\n\tmadc.lo.u32 %1, %3, %6, %5;"
+        : "=r"(l), "=r"(h)
+        : "r"(lo(a)), "r"(hi(a)), "r"(lo(b)), "r"(hi(b)), "r"(one));
+    return pack(l, h);
+  }
+  template <int B>
+  static __device__ __forceinline__ word shl_h(word x, uint32_t m /* opaque 2^B */) {
+    if constexpr (B >= 32) return pack(0u, lo(x) << (B - 32));
+    uint32_t l, h;
+    split(x, l, h);
+    return pack(l << B, madlo(h, m, mulhi(l, m)));
+  }
+  template <unsigned long long C>
+  static __device__ __forceinline__ word mulc_h(word x, uint32_t cq /* opaque (uint32_t)C */) {
+    uint32_t l, h;
+    split(x, l, h);
+    uint32_t nh = madlo(h, (uint32_t)C, mulhi(l, cq));
+    if constexpr ((C >> 32) != 0) nh = madlo(l, (uint32_t)(C >> 32), nh);
+    return pack(l * (uint32_t)C, nh);
   }
 };
 
@@ -244,8 +298,13 @@ struct Gen {
   //   bit 0: engine rotation by A (xoroshiro) / by B (xoshiro)
   //   bit 1: engine rotation by C (xoroshiro)
   //   bit 2: scrambler rotation by R (++ and **)
+  //   bit 3: the engine's constant left shift (high word through IMAD.HI)
+  //   bit 4: scrambler multiplies (* and **; high word through IMAD.HI)
+  //   bit 5: scrambler additions (+ and ++; high word as IMAD.X)
   static constexpr int kSites = (W == 64 ? ((FAM == SLP_FAM_XOROSHIRO ? 3 : (FAM == SLP_FAM_XOSHIRO ? 1 : 0)) |
-                                            ((SC == SLP_SC_PLUSPLUS || SC == SLP_SC_STARSTAR) ? 4 : 0))
+                                            ((SC == SLP_SC_PLUSPLUS || SC == SLP_SC_STARSTAR) ? 4 : 0) | 8 |
+                                            ((SC == SLP_SC_STAR || SC == SLP_SC_STARSTAR) ? 16 : 0) |
+                                            ((SC == SLP_SC_PLUS || SC == SLP_SC_PLUSPLUS) ? 32 : 0))
                                          : 0);
 
   // ALU/FMA instructions per output outside the rotation sites (SASS counts, profiles/)
@@ -300,12 +359,34 @@ struct Gen {
 
   template <int M, int RR>
   __device__ __forceinline__ word rot(word x) const {
-    if constexpr (M != 0 && SLP_ROT_POLICY == 2)
-      return O::template rotl_h<RR>(x, one << (RR & 31), one2 << (RR & 31));
-    else if constexpr (M != 0)
+    if constexpr (M != 0 && SLP_ROT_POLICY == 1)
       return O::template rotl_f<RR>(x);
+    else if constexpr (M != 0)
+      return O::template rotl_h<RR>(x, one << (RR & 31), one2 << (RR & 31));
     else
       return O::template rotl<RR>(x);
+  }
+  // constant shift / multiply sites (mask bits 8 and 16 = FMA-pipe form)
+  template <int M, int BB>
+  __device__ __forceinline__ word shl(word x) const {
+    if constexpr (M != 0)
+      return O::template shl_h<BB>(x, one << (BB & 31));
+    else
+      return O::template shl<BB>(x);
+  }
+  template <int M>
+  __device__ __forceinline__ word add(word a, word b) const {
+    if constexpr (M != 0)
+      return O::add_x(a, b, one);
+    else
+      return (word)(a + b);
+  }
+  template <int M, unsigned long long CC>
+  __device__ __forceinline__ word mulc(word x) const {
+    if constexpr (M != 0)
+      return O::template mulc_h<CC>(x, one2 * (uint32_t)CC);
+    else
+      return O::template mulc<CC>(x);
   }
 
   // register slot of flat word j when the ring offset is o (constant after unrolling)
@@ -318,13 +399,13 @@ struct Gen {
     if constexpr (SC == SLP_SC_NONE) {
       return xi;
     } else if constexpr (SC == SLP_SC_PLUS) {
-      return (word)(xi + s[slot(o, WJ)]);
+      return add<M & 32>(xi, s[slot(o, WJ)]);
     } else if constexpr (SC == SLP_SC_STAR) {
-      return O::template mulc<S_>(xi);
+      return mulc<M & 16, S_>(xi);
     } else if constexpr (SC == SLP_SC_PLUSPLUS) {
-      return (word)(rot<M & 4, R_>((word)(xi + s[slot(o, WJ)])) + xi);
+      return add<M & 32>(rot<M & 4, R_>(add<M & 32>(xi, s[slot(o, WJ)])), xi);
     } else {
-      return O::template mulc<T_>(rot<M & 4, R_>(O::template mulc<S_>(xi)));
+      return mulc<M & 16, T_>(rot<M & 4, R_>(mulc<M & 16, S_>(xi)));
     }
   }
 
@@ -336,15 +417,15 @@ struct Gen {
       const int i0 = slot(o, 0), il = slot(o, K - 1);
       const word x0 = s[i0];
       const word xl = s[il] ^ x0;
-      s[il] = rot<M & 1, A>(x0) ^ xl ^ O::template shl<B>(xl);
+      s[il] = rot<M & 1, A>(x0) ^ xl ^ shl<M & 8, B>(xl);
       s[i0] = rot<M & 2, C>(xl);
     } else if constexpr (FAM == SLP_FAM_XORSHIFT) {
       const int i0 = slot(o, 0), i1 = slot(o, 1);
       const word s0 = s[i0], s1 = s[i1];
-      const word t = s0 ^ O::template shl<A>(s0);
+      const word t = s0 ^ shl<M & 8, A>(s0);
       s[i0] = t ^ O::template shr<B>(t) ^ s1 ^ O::template shr<C>(s1);
     } else if constexpr (K == 4) {
-      const word t = O::template shl<A>(s[1]);
+      const word t = shl<M & 8, A>(s[1]);
       s[2] ^= s[0];
       s[3] ^= s[1];
       s[1] ^= s[2];
@@ -352,7 +433,7 @@ struct Gen {
       s[2] ^= t;
       s[3] = rot<M & 1, B>(s[3]);
     } else {
-      const word t = O::template shl<A>(s[1]);
+      const word t = shl<M & 8, A>(s[1]);
       s[2] ^= s[0];
       s[5] ^= s[1];
       s[1] ^= s[2];
@@ -426,6 +507,7 @@ struct GenR {
     g.T = (word)p.T;
     return g;
   }
+  static constexpr int kSites = 0;  // run-time parameters: every site in its ALU form
   static __host__ __device__ constexpr int best_mask(int, int) { return 0; }
   static __device__ __forceinline__ constexpr int slot(int o, int j) { return ring ? (o + j) % K : j; }
 
