@@ -205,9 +205,17 @@ __device__ __forceinline__ void reduce_checksum_block(uint64_t slo, uint64_t shi
 // FMA-form site mask of the generator inside k_fill (even / odd outputs).
 // Build knobs for A/B: SLP_FILL_MASK[2] (every kind), SLP_FILLC_MASK[2]
 // (converted and store + checksum kinds only: the generation-bound ones).
+// Default (measured, profiles/round2_ab_fused_sites.md): the ++ scrambler's
+// additions with IMAD.X high words (site 32) where generation bounds the fill
+// -- store + checksum (+6-7%) and the 8- and 16-word engines (xoshiro512++
+// store +3%, converted +5%); everything else keeps the all-ALU forms (the
+// HBM-bound native store loses 9% with IMAD.HI multiplies).
 template <class G, int OK, bool CSUM>
 __host__ __device__ constexpr int fill_site_mask(int odd) {
   int m = G::best_mask(0, 0), m2 = m;
+  if constexpr (!G::runtime) {
+    if (G::w == 64 && G::sc == SLP_SC_PLUSPLUS && (CSUM || G::k >= 8)) m = m2 = 32;
+  }
 #ifdef SLP_FILL_MASK
   m = m2 = SLP_FILL_MASK;
 #ifdef SLP_FILL_MASK2

@@ -21,10 +21,18 @@ constexpr int kFusedThreads = 256;
 // pipe -- IMAD.HI and IMAD.WIDE add to its time (profiles/int_peak.cu mixes)
 // -- so rotations and shifts stay ALU forms (every FMA form lost 1-25%).  The
 // scrambler multiplies do better as IMAD + IMAD + IMAD.HI (site 16) than as
-// IMAD.WIDE + IMAD: +1..4%, except the two cases below (-1%).
+// IMAD.WIDE + IMAD: +1..4%, except the two cases below (-1%); and the
+// scrambler additions' high words as IMAD.X (site 32), which is a plain IMAD
+// with a carry-in and runs beside the ALU pipe.
 template <class G, bool MANT, bool F64>
 __host__ __device__ constexpr int fused_site_mask() {
-  if constexpr (G::runtime || !(G::kSites & 16)) {
+  if constexpr (G::runtime) {
+    return 0;
+  } else if constexpr ((G::kSites & 32) != 0) {
+    // + / ++: the additions' high words as IMAD.X (site 32): ++ gains 4-6%
+    // (sum + xor) and 9-12% (exact, + f64); + gains 2-3% in the exact modes
+    return (G::sc == SLP_SC_PLUSPLUS || MANT) ? 32 : 0;
+  } else if constexpr (!(G::kSites & 16)) {
     return G::best_mask(1, (G::w == 64 ? 2 : 1) + (MANT ? 1 : 0));
   } else {
     if (G::fam == SLP_FAM_XOSHIRO && G::k == 8 && !MANT) return 0;                                // xoshiro512**, sum + xor
