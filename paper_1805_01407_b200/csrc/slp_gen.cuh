@@ -64,6 +64,13 @@ __device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {
 //            Gen::best_mask with SLP_ROT_POLICY=1 loses to IMAD.WIDE's rate)
 //   shl    : IMAD.SHL (low half) + SHF.L.U64.HI          -> 1 FMA + 1 ALU
 //   mulc   : IMAD.WIDE + IMAD (+ IMAD for a 64-bit constant).
+// Pipe-overlap mixes in the same file (round 2): only PLAIN IMADs (IMAD,
+// IMAD.SHL, IMAD.IADD, IMAD.X) run beside ALU instructions; IMAD.HI and
+// IMAD.WIDE add ~0.5-0.65 / ~1.75 SM cycles per warp instruction to the ALU
+// pipe's time.  Hence the *_h forms below (IMAD.HI carries) only pay where
+// they replace an IMAD.WIDE (mulc_h), never where they replace one SHF
+// (rotl_h, shl_h: A/B knobs only); add_x (IADD3 + IMAD.X) always pays in
+// ALU-bound kernels.  See profiles/round2_ab_fused_sites.md.
 #ifndef SLP_ROTH_FORM
 #define SLP_ROTH_FORM 0  // rotl_h low halves: 1 constant shifts + mad.hi, 0 mul.hi + mad.lo by an opaque 2^r
 #endif
@@ -256,8 +263,11 @@ struct WOps<64> {
 // Build-time policy switches (A/B experiments, profiles/): rotation pipe
 // balancing and the fused accumulator form.
 #ifndef SLP_ROT_POLICY
-// 0: all rotations on the ALU; 1: Gen::best_mask with 3-IMAD.WIDE rotations
-// (A/B: slower); 2: Gen::best_mask with IMAD + IMAD.HI rotations (rotl_h)
+// what Gen::best_mask proposes for the rotation sites: 0: all rotations on
+// the ALU; 1: 3-IMAD.WIDE rotations (rotl_f; A/B: slower); 2: IMAD + IMAD.HI
+// rotations (rotl_h; A/B: slower).  A site mask forced by a kernel
+// (SLP_FUSED_MASK / SLP_FILL_MASK, fused_site_mask, fill_site_mask) uses
+// rotl_h for its rotation bits unless the policy is 1.
 #define SLP_ROT_POLICY 0
 #endif
 #ifndef SLP_SUM_POLICY
