@@ -1,6 +1,8 @@
 // Kernels K1 (polynomial jump, k_jump) and K1t (table-driven jump, k_jump_table) and their launchers.
 #pragma once
 
+#include <cstdlib>
+
 #include "slp_gen.cuh"
 
 namespace slp {
@@ -15,13 +17,31 @@ namespace dev {
 
 constexpr int kJumpThreads = 128;
 
+inline int env_int_jump(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// Wide engines (k >= 8) with few states are bound by the latency of one
+// thread's n dependent steps (2^15 xoroshiro1024 jumps: 52-59 us per launch,
+// profiles/round2_init1024_launches.csv).  p.parts > 1 splits one jump over
+// `parts` adjacent lanes: lane q first steps its copy q * n / parts times
+// without accumulating (~10 instructions per step instead of ~45), then
+// handles coefficients [q * n / parts, (q + 1) * n / parts); the partial sums
+// are xor-ed with shuffles.  More total work, a 2-3x shorter critical path.
 template <class G, bool UNIFORM>
 __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __grid_constant__ BaseStates base) {
   const G eng = G::load(p.rt);
   using word = typename G::word;
   constexpr int K = G::k;
-  uint64_t t = (uint64_t)blockIdx.x * kJumpThreads + threadIdx.x;
-  if (t >= p.count) return;
+  constexpr bool SPLIT = K >= 8;  // p.parts is honoured (jump_impl only sets it for these)
+  const uint32_t parts = SPLIT ? (p.parts ? p.parts : 1u) : 1u;
+  const uint64_t gt = (uint64_t)blockIdx.x * kJumpThreads + threadIdx.x;
+  uint64_t t = SPLIT ? gt / parts : gt;
+  const uint32_t part = SPLIT ? (uint32_t)(gt - t * parts) : 0u;
+  const bool live = t < p.count;
+  if (!SPLIT && !live) return;
+  if (!live) t = 0;  // split: the lanes of a warp stay together for the shuffles (results discarded)
   uint64_t b = blockIdx.y;
   if (p.fold) {  // few states per batch: fold the batches into x so the warps are full
     b = t / p.fold;
@@ -49,8 +69,23 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __gri
   // few warps run (segment split, direct launches).  16 is a multiple of the
   // ring length, so the register rotation stays static.
   constexpr int UB = K >= 8 ? 16 : 64;
+  int w0 = 0, w1 = pw_used;
+  if constexpr (SPLIT) {
+    if (parts > 1) {
+      const int wpp = G::pw / (int)parts;  // polynomial words per part (parts divides pw)
+      w0 = (int)part * wpp;
+      w1 = w0 + wpp < pw_used ? w0 + wpp : pw_used;
+      if (w0 < w1) {  // advance to x^(64 * w0) without accumulating
 #pragma unroll 1
-  for (int wi = 0; wi < pw_used; ++wi) {
+        for (int c = 0; c < w0 * (64 / UB); ++c) {
+#pragma unroll
+          for (int bb = 0; bb < UB; ++bb) eng.step(cur, bb % K);
+        }
+      }
+    }
+  }
+#pragma unroll 1
+  for (int wi = w0; wi < w1; ++wi) {
     uint64_t cb = poly[wi];
 #pragma unroll 1
     for (int c = 0; c < 64; c += UB, cb >>= (UB & 63)) {
@@ -70,6 +105,13 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __gri
         eng.step(cur, o);
       }
     }
+  }
+  if constexpr (SPLIT) {
+    for (uint32_t off = 1; off < parts; off <<= 1) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[j] ^= __shfl_xor_sync(0xffffffffu, acc[j], off);
+    }
+    if (!live || part != 0) return;
   }
   word *dst = static_cast<word *>(p.dst);
   const uint64_t di = b * p.batch_stride + p.dst_off + t;
@@ -192,15 +234,37 @@ __global__ void __launch_bounds__(kTableThreads) k_jump_table(TableJumpParams p,
 template <class G>
 int jump_impl(const JumpParams &p, const BaseStates *base, bool uniform, uint64_t nbatch, cudaStream_t st) {
   if (p.count == 0 || nbatch == 0) return SLP_OK;
-  const uint64_t gx = (p.count + kJumpThreads - 1) / kJumpThreads;
+  JumpParams q = p;
+  q.parts = 1;
+  if constexpr (G::k >= 8) {
+    // split each jump over lanes while the launch is far from filling the GPU
+    // (SLP_JUMP_PARTS: 0 auto, 1 off, 2/4/8 forced; A/B)
+    static const int forced = env_int_jump("SLP_JUMP_PARTS", 0);
+    const uint64_t total = p.count * nbatch;
+    uint32_t parts = 1;
+    if (forced == 2 || forced == 4 || forced == 8)
+      parts = (uint32_t)forced;
+    else if (forced == 0) {
+      // measured (profiles/round2_jump_parts.md): the 16-word ring engine, whose
+      // step is ~4x cheaper than the accumulate, wants 4 lanes up to 2^17
+      // jumps; xoshiro512's step costs as much as half an accumulate: 2 lanes
+      if (G::k >= 16)
+        parts = total <= (1ull << 13) ? 8u : (total <= (1ull << 17) ? 4u : (total <= (1ull << 18) ? 2u : 1u));
+      else
+        parts = total <= (1ull << 12) ? 8u : (total <= (1ull << 13) ? 4u : (total <= (1ull << 17) ? 2u : 1u));
+    }
+    while (parts > 1 && (G::pw % (int)parts) != 0) parts >>= 1;
+    q.parts = parts;
+  }
+  const uint64_t gx = (p.count * q.parts + kJumpThreads - 1) / kJumpThreads;
   if (gx > 0x7fffffffull || nbatch > 65535) return SLP_ERR_INVALID;
   dim3 grid((unsigned)gx, (unsigned)nbatch);
   static BaseStates zero_base;  // unused when p.use_base == 0
   const BaseStates &bs = base ? *base : zero_base;
   if (uniform)
-    k_jump<G, true><<<grid, kJumpThreads, 0, st>>>(p, bs);
+    k_jump<G, true><<<grid, kJumpThreads, 0, st>>>(q, bs);
   else
-    k_jump<G, false><<<grid, kJumpThreads, 0, st>>>(p, bs);
+    k_jump<G, false><<<grid, kJumpThreads, 0, st>>>(q, bs);
   return check_launch("k_jump");
 }
 

@@ -73,6 +73,7 @@ struct JumpParams {
   uint64_t src_batch_stride;  // source states per batch (0: batch_stride)
   uint64_t fold;              // > 0: batches folded into t (batch t / fold, index t % fold), grid.y = 1
   int pw_used;            // polynomial words actually used (0 = all); trims the loop for low-degree polys
+  uint32_t parts;         // lanes per jump (k_jump's latency split; set by jump_impl, 0 = 1)
   GenRt rt;                // run-time generator parameters (custom engines)
 };
 
