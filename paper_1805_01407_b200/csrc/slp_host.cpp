@@ -17,6 +17,7 @@
 #include <map>
 #include <memory>
 #include <stdexcept>
+#include <thread>
 #include <tuple>
 
 #include "../../include/slp_b200.h"
@@ -561,6 +562,22 @@ static uint64_t plan_direct(int nbits) {
   if (env > 0) return (uint64_t)env;
   return nbits <= 256 ? kDirect : (nbits <= 512 ? kDirect / 4 : kDirect / 8);
 }
+// Requests beyond the small direct set of a wide engine get 4096 direct
+// polynomials (SLP_PLAN_DIRECT_BIG overrides): since K1 splits a wide jump
+// over lanes, one launch of 4096 per-lane-polynomial jumps costs less than
+// the radix-8 rounds it replaces (xoroshiro1024: 2^15 substreams 0.160 ->
+// 0.088 ms, one stream of 2^28 outputs 4.29 -> 5.0 TB/s;
+// profiles/round2_jump_parts.md).  Their host cost (one degree-n mulmod
+// each, ~4.4 us for n = 1024) is spread over threads in init_plan.
+static uint64_t plan_direct_big(int nbits) {
+  static const long env = [] {
+    const char *v = std::getenv("SLP_PLAN_DIRECT_BIG");
+    return v && *v ? std::atol(v) : 0L;
+  }();
+  const uint64_t small = plan_direct(nbits);
+  if (env > 0) return (uint64_t)env > small ? (uint64_t)env : small;
+  return nbits <= 256 ? small : 4096;
+}
 static constexpr uint64_t kRadix = 8;
 
 struct PlanKey {
@@ -593,7 +610,7 @@ std::shared_ptr<const InitPlan> init_plan(int id, const uint64_t *steps, int ste
   // caller with many different counts (HWD ranges) shares O(log n) plans and
   // their device tables instead of one per count.
   const GenDesc &gd = *gen_desc(eid);
-  const uint64_t nd = plan_direct(gd.n());
+  const uint64_t nd = n_req <= plan_direct(gd.n()) ? plan_direct(gd.n()) : plan_direct_big(gd.n());
   uint64_t n = nd;
   while (n < n_req) n *= kRadix;
   PlanKey key{eid, st, n};
@@ -617,17 +634,48 @@ std::shared_ptr<const InitPlan> init_plan(int id, const uint64_t *steps, int ste
   const Reducer red(P);
   // fewer direct polynomials for wide engines: each costs a host mulmod of
   // degree-n polys (plan build time), the rounds that replace them are cheap
-  const uint64_t ndirect = plan_direct(g.n());
-  const uint64_t m0 = n < ndirect ? n : ndirect;
-  // launch 0: x^(iJ) for i < m0
+  const uint64_t m0 = nd;  // n = nd * 8^r
+  // launch 0: x^(iJ) for i < m0.  A long chain is cut into blocks: the block
+  // starts x^(kBJ) come from x^(BJ) (square-and-multiply), then one thread per
+  // block multiplies by x^J.
   Poly cur{1};
   cur = poly_mod(cur, P);
-  std::vector<Poly> direct;
-  for (uint64_t i = 0; i < m0; ++i) {
-    direct.push_back(cur);
-    push(cur);
-    cur = red.mulmod(cur, xJ);
+  std::vector<Poly> direct(m0);
+  unsigned nthr = std::thread::hardware_concurrency();
+  if (nthr > 16) nthr = 16;
+  if (m0 < 1024 || nthr < 2) {
+    for (uint64_t i = 0; i < m0; ++i) {
+      direct[i] = cur;
+      cur = red.mulmod(cur, xJ);
+    }
+  } else {
+    const uint64_t B = (m0 + nthr - 1) / nthr;
+    Poly xBJ{1}, sq = xJ;  // x^(BJ)
+    for (uint64_t e = B; e; e >>= 1) {
+      if (e & 1) xBJ = red.mulmod(xBJ, sq);
+      if (e > 1) sq = red.mulmod(sq, sq);
+    }
+    std::vector<Poly> starts;
+    for (uint64_t lo = 0; lo < m0; lo += B) {
+      starts.push_back(cur);
+      cur = red.mulmod(cur, xBJ);
+    }
+    std::vector<Poly> ends(starts.size());
+    std::vector<std::thread> pool;
+    for (size_t k = 0; k < starts.size(); ++k)
+      pool.emplace_back([&, k] {
+        Poly c = starts[k];
+        const uint64_t lo = k * B, hi = lo + B < m0 ? lo + B : m0;
+        for (uint64_t i = lo; i < hi; ++i) {
+          direct[i] = c;
+          c = red.mulmod(c, xJ);
+        }
+        ends[k] = c;
+      });
+    for (auto &t : pool) t.join();
+    cur = ends.back();  // x^(m0 J)
   }
+  for (uint64_t i = 0; i < m0; ++i) push(direct[i]);
   plan->launches.push_back(InitLaunch{0, m0, 0, 0, false});
   // x^(m0 J) is `cur` now
   uint64_t m = m0;

@@ -27,8 +27,8 @@ def timeit(fn, reps=5):
     return best
 
 
-mode = os.environ.get("SLP_JUMP_PARTS", "auto")
-for name in ["xoroshiro1024starstar", "xoroshiro1024plusplus", "xoshiro512starstar", "xoshiro256starstar"]:
+mode = os.environ.get("SLP_JUMP_PARTS", "auto") + ("/direct=" + os.environ["SLP_PLAN_DIRECT"] if os.environ.get("SLP_PLAN_DIRECT") else "")
+for name in (sys.argv[1:] or ["xoroshiro1024starstar", "xoroshiro1024plusplus", "xoshiro512starstar", "xoshiro256starstar"]):
     spec = P.get_spec(name)
     for T in (1 << 28, 1 << 24):
         one = D.Substreams.from_seed(spec, 42, 1)
