@@ -108,6 +108,15 @@ int slp_char_poly(int id, uint64_t *poly, int poly_words);
 /* x^steps mod P, steps a little-endian multiword integer; replaces
  * compute_jump_poly (generators.py:397-402, gf2.py:214-227). */
 int slp_jump_poly(int id, const uint64_t *steps, int steps_words, uint64_t *poly, int poly_words);
+/* Polynomial `index` of the substream-initialisation plan slp_init_substreams
+ * uses for `n` substreams `steps` apart: the plan starts with x^(i*steps) mod P
+ * for i < direct (one K1 jump per substream; the doubling of
+ * LanedStream.__init__, generators.py:443-456, done with jump polynomials),
+ * followed by the polynomials of its radix-8 rounds.  Returns the number of
+ * polynomials in the plan, or a negative status; `poly` may be NULL.  Host
+ * only -- lets tests check a plan against slp_jump_poly without a GPU. */
+int64_t slp_init_plan_poly(int id, const uint64_t *steps, int steps_words, uint64_t n, uint64_t index,
+                           uint64_t *poly, int poly_words);
 /* scalar jump of one flat state (k words, each < 2^w) on the host; replaces
  * Generator.jump (generators.py:315-334). */
 int slp_host_jump(int id, const uint64_t *poly, int poly_words, uint64_t *flat_state);

@@ -70,6 +70,8 @@ SIGNATURES = {
     "slp_register_generator": (ctypes.c_int, [ctypes.POINTER(GenInfo)]),
     "slp_char_poly": (ctypes.c_int, [ctypes.c_int, u64p, ctypes.c_int]),
     "slp_jump_poly": (ctypes.c_int, [ctypes.c_int, u64p, ctypes.c_int, u64p, ctypes.c_int]),
+    "slp_init_plan_poly": (ctypes.c_int64, [ctypes.c_int, u64p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, u64p,
+                                            ctypes.c_int]),
     "slp_host_jump": (ctypes.c_int, [ctypes.c_int, u64p, ctypes.c_int, u64p]),
     "slp_engine_char_poly": (ctypes.c_int, [ctypes.c_int] * 6 + [u64p, ctypes.c_int]),
     "slp_engine_jump_poly": (ctypes.c_int, [ctypes.c_int] * 6 + [u64p, ctypes.c_int, u64p, ctypes.c_int]),

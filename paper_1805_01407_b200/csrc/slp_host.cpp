@@ -789,6 +789,28 @@ int slp_jump_poly(int id, const uint64_t *steps, int steps_words, uint64_t *poly
   }
 }
 
+int64_t slp_init_plan_poly(int id, const uint64_t *steps, int steps_words, uint64_t n, uint64_t index,
+                           uint64_t *poly, int poly_words) {
+  if (!gen_desc(id)) return SLP_ERR_UNKNOWN_GENERATOR;
+  if (steps_words < 0 || (steps_words > 0 && !steps) || n == 0) return SLP_ERR_INVALID;
+  try {
+    const auto plan = init_plan(id, steps, steps_words, n);
+    const uint64_t count = plan->polys.size() / (uint64_t)plan->pw;
+    if (poly && index < count) {
+      if (poly_words < plan->pw) return SLP_ERR_INVALID;
+      for (int i = 0; i < poly_words; ++i)
+        poly[i] = i < plan->pw ? plan->polys[index * (uint64_t)plan->pw + (uint64_t)i] : 0;
+    }
+    return (int64_t)count;
+  } catch (const AlgebraError &e) {
+    set_last_error(e.what());
+    return SLP_ERR_ALGEBRA;
+  } catch (const std::exception &e) {
+    set_last_error(e.what());
+    return SLP_ERR_INVALID;
+  }
+}
+
 int slp_host_jump(int id, const uint64_t *poly, int poly_words, uint64_t *flat_state) {
   const GenDesc *g = gen_desc(id);
   if (!g) return SLP_ERR_UNKNOWN_GENERATOR;

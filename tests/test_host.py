@@ -187,6 +187,51 @@ def test_ring_pointer_forms_agree():
     assert outs == ref
 
 
+@pytest.mark.parametrize("name,n,stride", [
+    ("xoroshiro1024plusplus", 100, 1 << 512),      # small plan: 128 direct polynomials
+    ("xoroshiro1024plusplus", 5000, 1 << 512),     # big plan: 4096 direct (threaded build), then rounds
+    ("xoshiro512starstar", 40000, (1 << 256) + 12345),
+    ("xoshiro256starstar", 3000, 1 << 128),
+    ("xoroshiro64starstar", 3000, 977),
+])
+def test_init_plan_polynomials(name, n, stride):
+    """The substream-initialisation plan (slp_init_substreams) holds x^(i*stride)
+    mod P for i < direct, then the radix-8 round polynomials x^(c*m*stride):
+    checked against compute_jump_poly (generators.py:397-402), including the
+    block boundaries of the threaded build of large plans."""
+    spec = P.get_spec(name)
+    gid = _native.lib().slp_generator_id(name.encode())
+    sw, sn = _native.int_to_words(stride)
+    pw = (spec.kind.n + 63) // 64
+    buf = (ctypes.c_uint64 * pw)()
+
+    def plan_poly(i):
+        cnt = _native.lib().slp_init_plan_poly(gid, sw, sn, n, i, buf, pw)
+        assert cnt > 0
+        return cnt, _native.words_to_int(buf)
+
+    count, p0 = plan_poly(0)
+    assert p0 == 1
+    small = {256: 1024, 512: 256, 1024: 128}.get(spec.kind.n, 1024)
+    direct = small if n <= small or spec.kind.n <= 256 else 4096
+    direct = min(direct, count)
+    rng = random.Random(n)
+    idx = {1, 2, direct - 1, direct // 2, direct // 2 - 1, direct // 2 + 1} | {direct * j // 16 for j in range(1, 16)} \
+        | {direct * j // 16 - 1 for j in range(1, 16)} | {direct * j // 8 + 1 for j in range(1, 8)} \
+        | {rng.randrange(direct) for _ in range(8)}
+    for i in sorted(i for i in idx if 0 <= i < direct):
+        assert plan_poly(i)[1] == P.compute_jump_poly(spec, i * stride).poly.bits, (name, i)
+    # the rounds (plans are built for direct * 8^r >= n): 7 polynomials x^(c * m * stride) each
+    m, at = direct, direct
+    while m < n:
+        for c in range(1, 8):
+            assert plan_poly(at)[1] == P.compute_jump_poly(spec, c * m * stride).poly.bits, (name, m, c)
+            at += 1
+        m *= 8
+    assert at == count
+    assert _native.lib().slp_init_plan_poly(gid, sw, sn, n, count + 5, None, 0) == count  # out of range: count only
+
+
 def test_native_host_jump_errors():
     L = _native.lib()
     st = (ctypes.c_uint64 * 4)(0, 0, 0, 0)
