@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kFusedThreads, SLP_FUSED_MINB) k_fused(FusedPa
   constexpr int MSK2 = MSK;
 #endif
   const uint32_t one = p.one;
+  (void)one;  // only the IMAD.WIDE accumulator policies (SLP_SUM_POLICY 1, 2) read it
   uint64_t slo = 0, shi = 0, sx = 0, slow = 0;
   double fs = 0.0, fs2 = 0.0;
   for (uint64_t u = (uint64_t)blockIdx.x * WPB + warp; u < p.nunits; u += (uint64_t)gridDim.x * WPB) {
