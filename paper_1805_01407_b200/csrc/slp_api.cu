@@ -586,11 +586,10 @@ static int poly_table_on_device(int id, int dev, const uint64_t *poly, cudaStrea
 constexpr uint64_t kJumpTableMinStates = 65536;
 
 static bool use_jump_tables(uint64_t count) {
-  static const long min_states = [] {  // SLP_INIT_TABLES=0 disables K1t; =N sets the threshold (A/B)
-    const char *v = std::getenv("SLP_INIT_TABLES");
-    if (v && *v == '0') return -1L;
-    return v && *v ? std::atol(v) : 16384L;
-  }();
+  // SLP_INIT_TABLES=0 disables K1t; =N sets the threshold (A/B).  Read on every
+  // call (a getenv per launch is noise) so that tests can switch it in-process.
+  const char *v = std::getenv("SLP_INIT_TABLES");
+  const long min_states = (v && *v == '0') ? -1L : (v && *v ? std::atol(v) : 16384L);
   return min_states >= 0 && count >= (uint64_t)min_states;
 }
 

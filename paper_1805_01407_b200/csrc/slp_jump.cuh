@@ -238,8 +238,8 @@ int jump_impl(const JumpParams &p, const BaseStates *base, bool uniform, uint64_
   q.parts = 1;
   if constexpr (G::k >= 8) {
     // split each jump over lanes while the launch is far from filling the GPU
-    // (SLP_JUMP_PARTS: 0 auto, 1 off, 2/4/8 forced; A/B)
-    static const int forced = env_int_jump("SLP_JUMP_PARTS", 0);
+    // (SLP_JUMP_PARTS: 0 auto, 1 off, 2/4/8 forced; A/B and tests -- read on every call)
+    const int forced = env_int_jump("SLP_JUMP_PARTS", 0);
     const uint64_t total = p.count * nbatch;
     uint32_t parts = 1;
     if (forced == 2 || forced == 4 || forced == 8)
