@@ -27,6 +27,18 @@ namespace dev {
 constexpr int kHwdThreads = 256;
 constexpr uint32_t kHwdRecip = 0x55555556u;  // ceil(2^32 / 3), hwd.py:44
 
+template <class G>
+__host__ __device__ constexpr int hwd_site_mask() {
+  if constexpr (G::runtime) {
+    return 0;
+  } else {
+    // measured (profiles/round2_ab_hwd_sites.jsonl): ++ +2.7..3.2%; ** +0.7% (xoshiro256),
+    // +1.9% (xoshiro512), -1.8% (xoroshiro128: keeps IMAD.WIDE)
+    if ((G::kSites & 32) && G::sc == SLP_SC_PLUSPLUS) return 32;
+    return ((G::kSites & 16) && G::fam == SLP_FAM_XOSHIRO) ? 16 : 0;
+  }
+}
+
 // counts one thread's segment; GLOBAL: 64-bit global atomics, else packed smem
 // cells.  SLICED: only signatures in [cell_lo, cell_lo + p.slice_cells) are
 // counted (3^k cells split over the CTAs of blockIdx.y); returns the number
@@ -102,14 +114,22 @@ __device__ __forceinline__ uint32_t hwd_segment(const HwdParams &p, uint64_t i, 
     consume(pend, true);
     --cnt;
   }
-  // phase B: counting in unrolled chunks of CH words (ring offsets static)
+  // phase B: counting in unrolled chunks of CH words (ring offsets static).
+  // The kernel is ALU-bound like K4, so the scrambler takes the same FMA-pipe
+  // forms (Gen::kSites: multiplies with IMAD.HI carries, ++ additions with
+  // IMAD.X high words; profiles/round2_ab_fused_sites.md).  SLP_HWD_MASK: A/B.
   constexpr int CH = 16;
+#ifdef SLP_HWD_MASK
+  constexpr int MSK = SLP_HWD_MASK & G::kSites;
+#else
+  constexpr int MSK = hwd_site_mask<G>();
+#endif
   constexpr uint32_t VPW = SPLIT ? 2 : 1;  // test values per generator word
   for (uint32_t c = cnt / (CH * VPW); c > 0; --c) {
 #pragma unroll
     for (int t = 0; t < CH; ++t) {
-      const word x = eng.output(s, t % K);
-      eng.step(s, t % K);
+      const word x = eng.template output_m<MSK>(s, t % K);
+      eng.template step_m<MSK>(s, t % K);
       if constexpr (SPLIT) {
         consume((uint64_t)x & 0xFFFFFFFFull, true);
         consume((uint64_t)x >> 32, true);
