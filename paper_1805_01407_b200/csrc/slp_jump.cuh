@@ -136,6 +136,18 @@ __global__ void __launch_bounds__(kJumpThreads) k_jump(JumpParams p, const __gri
 // (LDS.128 over 256-byte rows conflicts: entries v and v+8 share banks;
 // ncu counted ~3 extra wavefronts per load.)
 
+// Threads per K1t CTA.  A 1024-bit engine's table slice (128 KB) allows one
+// CTA per SM, and 8 warps do not cover the shared-memory latency: 512 threads
+// take 2^20 xoroshiro1024 states from 1.26 to 1.14 ms and 2^21 from 2.69 to
+// 2.18 ms; 1024 threads and the smaller engines (several CTAs per SM) lose
+// 3-10% (profiles/round2_k1t_threads.jsonl).
+#ifndef SLP_K1T_THREADS
+#define SLP_K1T_THREADS 256
+#endif
+#ifndef SLP_K1T_THREADS_WIDE
+#define SLP_K1T_THREADS_WIDE 512
+#endif
+
 template <class G>
 struct JumpTable {
   static constexpr int NB = G::n;              // state bits
@@ -146,10 +158,10 @@ struct JumpTable {
   static constexpr int Q = S / VW;             // vector loads per lookup
   static constexpr int NG = NB / 4;            // nibble groups
   static constexpr int slice_words = NG * 16 * S;
+  static constexpr int threads = NB >= 1024 ? SLP_K1T_THREADS_WIDE : SLP_K1T_THREADS;  // per CTA
   static constexpr uint64_t table_words = (uint64_t)Z * slice_words;  // n^2 / 8
   static_assert(NW * 32 == NB && NW % S == 0 && S % VW == 0, "table geometry");
 };
-constexpr int kTableThreads = 256;
 
 // 32-bit word j of state i in SoA [k][ld] storage of w-bit words
 template <class G>
@@ -178,8 +190,9 @@ __global__ void k_build_table(const void *rows, uint32_t *table) {
 }
 
 template <class G>
-__global__ void __launch_bounds__(kTableThreads) k_jump_table(TableJumpParams p, uint32_t cpc) {
+__global__ void __launch_bounds__(JumpTable<G>::threads) k_jump_table(TableJumpParams p, uint32_t cpc) {
   using JT = JumpTable<G>;
+  constexpr int kTableThreads = JT::threads;
   using word = typename G::word;
   using vec = uint2;
   extern __shared__ __align__(16) uint8_t tsm_raw[];
@@ -286,6 +299,7 @@ int jump_table_impl(const TableJumpParams &p, uint64_t nbatch, cudaStream_t st) 
   if (p.count == 0 || nbatch == 0) return SLP_OK;
   if (nbatch > 65535 || p.m == 0) return SLP_ERR_INVALID;
   constexpr int smem = JT::slice_words * 4;
+  constexpr int kTableThreads = JT::threads;
   auto kern = k_jump_table<G>;
   const int dev = current_device();
   static std::atomic<int> per_sm[64];  // occupancy per device (benign race: same value)
