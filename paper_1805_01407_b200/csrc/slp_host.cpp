@@ -17,6 +17,7 @@
 #include <map>
 #include <memory>
 #include <stdexcept>
+#include <system_error>
 #include <thread>
 #include <tuple>
 
@@ -661,17 +662,23 @@ std::shared_ptr<const InitPlan> init_plan(int id, const uint64_t *steps, int ste
       cur = red.mulmod(cur, xBJ);
     }
     std::vector<Poly> ends(starts.size());
+    auto work = [&](size_t k) {
+      Poly c = starts[k];
+      const uint64_t lo = k * B, hi = lo + B < m0 ? lo + B : m0;
+      for (uint64_t i = lo; i < hi; ++i) {
+        direct[i] = c;
+        c = red.mulmod(c, xJ);
+      }
+      ends[k] = c;
+    };
     std::vector<std::thread> pool;
-    for (size_t k = 0; k < starts.size(); ++k)
-      pool.emplace_back([&, k] {
-        Poly c = starts[k];
-        const uint64_t lo = k * B, hi = lo + B < m0 ? lo + B : m0;
-        for (uint64_t i = lo; i < hi; ++i) {
-          direct[i] = c;
-          c = red.mulmod(c, xJ);
-        }
-        ends[k] = c;
-      });
+    size_t spawned = 0;
+    try {
+      for (; spawned + 1 < starts.size(); ++spawned) pool.emplace_back(work, spawned);
+    } catch (const std::system_error &) {
+      // no more threads: the remaining blocks run here
+    }
+    for (size_t k = spawned; k < starts.size(); ++k) work(k);  // the last block (and any unspawned) inline
     for (auto &t : pool) t.join();
     cur = ends.back();  // x^(m0 J)
   }
